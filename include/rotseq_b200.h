@@ -1,0 +1,118 @@
+/*
+ * rotseq_b200 — C-ABI of the B200-native rotation-sequence apply.
+ *
+ * Drop-in boundary for the reference package `rotseq` (arXiv 2412.01852 artifact):
+ *
+ *   reference entry point                         replaced by
+ *   --------------------------------------------  ------------------------------------
+ *   rotseq.core.apply_naive(A, seq, kind, fast)    rs_apply_f64(..., side=0, order=0, ...)
+ *     /root/reference/pkg/src/rotseq/core.py:365-374
+ *   rotseq.blocking.apply_blocked(A, seq, plan,    rs_apply_f64(...)   (plan/shape/threads are
+ *     shape, kind, threads, fast, use_kernel)        CPU cache knobs; the GPU tiling is internal)
+ *     /root/reference/pkg/src/rotseq/blocking.py:420-476
+ *   rotseq.verification.run_variant("kernel",...)  run_variant("cuda", ...) in the Python mirror
+ *     /root/reference/pkg/src/rotseq/verification.py:50-85
+ *   rotseq.blocking._kernel_chunk (the hot loop)   rs_pipeline kernel (internal)
+ *     /root/reference/pkg/src/rotseq/blocking.py:342-397
+ *
+ * Semantics (reference core.py:1-16, 130-149, 195-205):
+ *   A is an m x n column-major matrix (element (i,j) at A[i + j*lda]).
+ *   C and S are (len-1) x k column-major with leading dimension ldcs, where len = n for
+ *   side = RS_SIDE_RIGHT and len = m for side = RS_SIDE_LEFT.
+ *   For p = 0..k-1 (sweeps, ascending) and j = 0..len-2 (ascending; descending when
+ *   order = RS_ORDER_REVERSE), the 2x2 transform with (c, s) = (C[j,p], S[j,p]) is
+ *   applied to the pair x = column j, y = column j+1 (right side) or x = row j,
+ *   y = row j+1 (left side):
+ *     rotation : x' = c*x + s*y ;  y' = c*y - s*x            (core.py:130-137)
+ *     reflector: w = s*(x+y) ; x' = w + (c-s)*x ; y' = w - (c+s)*y   (core.py:140-149)
+ *   strict != 0: plain IEEE mul/add in exactly that expression shape (no FMA
+ *   contraction) -> bit-identical to the reference's strict numba build (_jit.py:14).
+ *   strict == 0: FMA contraction allowed (the reference's "fast" build, _jit.py:15).
+ *
+ * All pointers are DEVICE pointers. Calls are asynchronous on `stream` (a cudaStream_t,
+ * NULL = legacy default stream) and thread-safe for distinct buffers / workspaces.
+ * The library never frees caller buffers. A, C, S are owned by the caller.
+ *
+ * Errors: functions return rs_status; rs_last_error() returns a thread-local message
+ * for the last failing call on the calling thread. The Python mirror maps RS_EINVAL to
+ * ValueError (the reference raises ValueError for every argument error, core.py:41-51,
+ * 110-117) and everything else to RuntimeError.
+ */
+#ifndef ROTSEQ_B200_H
+#define ROTSEQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RS_OK = 0,
+  RS_EINVAL = 1,       /* bad argument (shape, stride, enum, null pointer)        */
+  RS_ECUDA = 2,        /* CUDA runtime error (launch failure, no device, ...)     */
+  RS_ENOMEM = 3,       /* workspace too small / allocation failed                 */
+  RS_EUNSUPPORTED = 4  /* configuration this build does not provide               */
+} rs_status;
+
+enum { RS_SIDE_RIGHT = 0, RS_SIDE_LEFT = 1 };
+enum { RS_ORDER_FORWARD = 0, RS_ORDER_REVERSE = 1 };
+enum { RS_KIND_ROTATION = 0, RS_KIND_REFLECTOR = 1 };
+enum { RS_DTYPE_F64 = 0, RS_DTYPE_F32 = 1 };
+enum { RS_ALGO_PIPELINE = 0, RS_ALGO_NAIVE = 1 };
+
+/* Library / ABI version (major*10000 + minor*100 + patch). */
+int rs_version(void);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+const char* rs_last_error(void);
+
+/* Bytes of device workspace rs_apply_* needs for this problem (packed coefficients +
+ * inter-CTA progress flags). Passing workspace == NULL to rs_apply_* makes the library
+ * allocate (and stream-order free) it itself. Returns 0 on invalid arguments. */
+size_t rs_workspace_bytes(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype);
+
+/* Apply the rotation sequence (C, S) to A in place (see header comment).
+ * Replaces rotseq.core.apply_naive / rotseq.blocking.apply_blocked
+ * (core.py:365-374, blocking.py:420-476). */
+rs_status rs_apply_f64(double* A, int64_t m, int64_t n, int64_t lda,
+                       const double* C, const double* S, int64_t ldcs, int64_t k,
+                       int side, int order, int kind, int strict,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* fp32 instantiation (BASELINE config 4). Same contract; tolerance-checked against the
+ * reference run in fp64 on the same fp32-rounded inputs. */
+rs_status rs_apply_f32(float* A, int64_t m, int64_t n, int64_t lda,
+                       const float* C, const float* S, int64_t ldcs, int64_t k,
+                       int side, int order, int kind, int strict,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Same as rs_apply_* with an explicit algorithm: RS_ALGO_PIPELINE (the product
+ * register-window band pipeline) or RS_ALGO_NAIVE (one thread per row/column, plain
+ * sweep loop in global memory: the GPU restatement of _naive_py, core.py:195-205, kept
+ * as an independent second implementation for cross-checks). */
+rs_status rs_apply_algo_f64(int algo, double* A, int64_t m, int64_t n, int64_t lda,
+                            const double* C, const double* S, int64_t ldcs, int64_t k,
+                            int side, int order, int kind, int strict,
+                            void* workspace, size_t workspace_bytes, void* stream);
+rs_status rs_apply_algo_f32(int algo, float* A, int64_t m, int64_t n, int64_t lda,
+                            const float* C, const float* S, int64_t ldcs, int64_t k,
+                            int side, int order, int kind, int strict,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Launch geometry the pipeline would use for this problem on the current device
+ * (for benchmarks / roofline accounting). Any out-pointer may be NULL. */
+rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype,
+                       int* grid_ctas, int* warps_per_cta, int64_t* units, int* band_width,
+                       int* rows_per_tile, size_t* smem_bytes);
+
+/* Number of pipeline / pack / naive kernel launches issued by this library since
+ * process start (all threads). Used by bench.py to report gpu_launches. */
+int64_t rs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ROTSEQ_B200_H */

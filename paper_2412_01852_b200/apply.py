@@ -1,0 +1,228 @@
+"""Drop-in entry points: apply a rotation sequence to A on a B200.
+
+Reference operator API being replaced (same argument meaning, in-place update,
+``None`` return, ``ValueError`` on bad arguments):
+
+* ``apply_naive(A, seq, kind, fast)``              core.py:365-374
+* ``apply_blocked(A, seq, plan, shape, kind,
+  threads, fast, use_kernel)``                     blocking.py:420-476
+* ``apply_blocked_packed`` / resident-A mode       blocking.py:479-515
+
+``apply_cuda`` is the general form. ``A`` is either
+
+* a host ``numpy`` array (column-major float64/float32, row-block views with
+  ld > rows allowed): it is copied to the device, transformed, and copied back
+  into the caller's array (the end-to-end path), or
+* a CUDA ``torch.Tensor`` whose first stride is 1 (a column-major view): it is
+  transformed in place on the tensor's current stream (the resident path; PyTorch
+  only provides the buffer and the stream).
+
+The arithmetic runs only in the CUDA library (``_lib``); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    Order,
+    RotationSequence,
+    Side,
+    TransformKind,
+    _as_enum,
+    check_apply_args,
+    require_colmajor,
+)
+
+ALGOS = {"pipeline": _lib.ALGO_PIPELINE, "naive": _lib.ALGO_NAIVE}
+
+
+def _torch():
+    import torch  # noqa: PLC0415 - torch is plumbing, imported lazily
+
+    return torch
+
+
+def _is_tensor(x) -> bool:
+    try:
+        torch = _torch()
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _np_to_device(arr: np.ndarray, dtype, device):
+    """Column-major device copy of a 2-D host array (any strides)."""
+    torch = _torch()
+    rows, cols = arr.shape
+    host = torch.from_numpy(np.asarray(arr))
+    out = torch.empty_strided((rows, cols), (1, max(rows, 1)), dtype=dtype, device=device)
+    out.copy_(host.to(dtype) if host.dtype != dtype else host)
+    return out
+
+
+def _seq_arrays(seq, dtype, device):
+    """(C, S) as column-major device tensors of `dtype`."""
+    torch = _torch()
+    if isinstance(seq, RotationSequence):
+        C, S = seq.C, seq.S
+    else:
+        C, S = seq
+    out = []
+    for X, name in ((C, "C"), (S, "S")):
+        if _is_tensor(X):
+            if X.device != device or X.dtype != dtype or X.dim() != 2 or (X.shape[0] > 1 and X.stride(0) != 1):
+                X = X.to(device=device, dtype=dtype)
+                if X.shape[0] > 1 and X.stride(0) != 1:
+                    X = X.t().contiguous().t()
+            out.append(X)
+        else:
+            X = np.asarray(X)
+            if X.ndim != 2:
+                raise ValueError(f"{name} must be 2-D")
+            out.append(_np_to_device(X, dtype, device))
+    if tuple(out[0].shape) != tuple(out[1].shape):
+        raise ValueError(f"C and S must share a 2-D shape, got {tuple(out[0].shape)} vs {tuple(out[1].shape)}")
+    return out[0], out[1]
+
+
+def _seq_ncols(seq) -> int:
+    if isinstance(seq, RotationSequence):
+        return seq.n_cols
+    return int(seq[0].shape[0]) + 1
+
+
+def apply_device(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Side.RIGHT,
+                 order=Order.FORWARD, algo: str = "pipeline", workspace=None, stream=None) -> None:
+    """In-place apply on a CUDA tensor A (column-major view). Asynchronous on
+    ``stream`` (default: the current torch stream of A's device)."""
+    torch = _torch()
+    kind = _as_enum(kind, TransformKind, "kind")
+    side = _as_enum(side, Side, "side")
+    order = _as_enum(order, Order, "order")
+    if algo not in ALGOS:
+        raise ValueError(f"unknown algorithm {algo!r}; choose from {tuple(ALGOS)}")
+    if not _is_tensor(A) or not A.is_cuda:
+        raise ValueError("A must be a CUDA torch.Tensor for apply_device")
+    if A.dim() != 2:
+        raise ValueError("A must be a 2-D tensor")
+    if A.dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"A must have dtype float64 or float32, got {A.dtype}")
+    m, n = int(A.shape[0]), int(A.shape[1])
+    if m > 1 and A.stride(0) != 1:
+        raise ValueError("A must be column-major (first stride 1); use A.t().contiguous().t()")
+    length = m if side is Side.LEFT else n
+    what = "rows" if side is Side.LEFT else "columns"
+    if length < 2:
+        if side is Side.LEFT:
+            raise ValueError(f"matrix needs at least 2 rows for left-side application, got {m}")
+        raise ValueError(f"matrix needs at least 2 columns, got {n}")
+    ncols = _seq_ncols(seq)
+    if ncols != length:
+        raise ValueError(f"sequence acts on {ncols} {what} but matrix has {length}")
+    if m == 0 or n == 0:
+        return
+    lda = int(A.stride(1)) if n > 1 else max(m, 1)
+    C, S = _seq_arrays(seq, A.dtype, A.device)
+    rows_cs, k = int(C.shape[0]), int(C.shape[1])
+    if rows_cs != length - 1:
+        raise ValueError(f"C/S have {rows_cs} rows, expected {length - 1}")
+
+    def _compact(X):
+        out = torch.empty_strided((rows_cs, k), (1, max(rows_cs, 1)), dtype=X.dtype, device=X.device)
+        out.copy_(X)
+        return out
+
+    ldc = int(C.stride(1)) if k > 1 else max(rows_cs, 1)
+    lds = int(S.stride(1)) if k > 1 else max(rows_cs, 1)
+    col_major = all(X.shape[0] <= 1 or X.stride(0) == 1 for X in (C, S))
+    if not col_major or ldc != lds or ldc < rows_cs:
+        C, S = _compact(C), _compact(S)
+        ldc = max(rows_cs, 1)
+    ldcs = ldc
+    lib = _lib.load()
+    f64 = A.dtype == torch.float64
+    dt = _lib.DTYPE_F64 if f64 else _lib.DTYPE_F32
+    side_i = _lib.SIDE_LEFT if side is Side.LEFT else _lib.SIDE_RIGHT
+    kind_i = _lib.KIND_REFLECTOR if kind is TransformKind.REFLECTOR else _lib.KIND_ROTATION
+    order_i = _lib.ORDER_REVERSE if order is Order.REVERSE else _lib.ORDER_FORWARD
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        need = lib.rs_workspace_bytes(m, n, k, side_i, kind_i, dt)
+        if workspace.numel() * workspace.element_size() < need:
+            raise ValueError(f"workspace too small: need {need} bytes")
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    if stream is None:
+        stream = torch.cuda.current_stream(A.device)
+    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    with torch.cuda.device(A.device):
+        fn = lib.rs_apply_algo_f64 if f64 else lib.rs_apply_algo_f32
+        st = fn(ALGOS[algo], A.data_ptr(), m, n, lda, C.data_ptr(), S.data_ptr(), ldcs, k,
+                side_i, order_i, kind_i, 0 if fast else 1, ws_ptr, ws_bytes, sptr)
+    # C/S may be temporaries from torch's caching allocator: tie them to the launch stream
+    if hasattr(stream, "cuda_stream") and stream != torch.cuda.current_stream(A.device):
+        C.record_stream(stream)
+        S.record_stream(stream)
+    _lib.check(st, "rs_apply")
+
+
+def workspace_bytes(m: int, n: int, k: int, side=Side.RIGHT, kind=TransformKind.ROTATION,
+                    dtype=np.float64) -> int:
+    side = _as_enum(side, Side, "side")
+    kind = _as_enum(kind, TransformKind, "kind")
+    lib = _lib.load()
+    dt = _lib.DTYPE_F64 if np.dtype(dtype) == np.float64 else _lib.DTYPE_F32
+    return int(lib.rs_workspace_bytes(m, n, k, _lib.SIDE_LEFT if side is Side.LEFT else _lib.SIDE_RIGHT,
+                                      _lib.KIND_REFLECTOR if kind is TransformKind.REFLECTOR else _lib.KIND_ROTATION,
+                                      dt))
+
+
+def apply_cuda(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Side.RIGHT,
+               order=Order.FORWARD, algo: str = "pipeline", device=None, workspace=None) -> None:
+    """Apply the sequence to A in place on the GPU; returns None.
+
+    Host numpy input: validated like the reference (``_check_apply_args``,
+    core.py:110-117), copied to ``device`` (default cuda:current), transformed,
+    copied back, synchronised. Device tensor input: see ``apply_device``.
+    """
+    if _is_tensor(A):
+        apply_device(A, seq, kind, fast, side, order, algo, workspace)
+        return
+    torch = _torch()
+    kind = _as_enum(kind, TransformKind, "kind")
+    side = _as_enum(side, Side, "side")
+    order = _as_enum(order, Order, "order")
+    if isinstance(seq, RotationSequence):
+        check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
+    else:
+        require_colmajor(A, dtypes=(np.float64, np.float32))
+    if A.shape[0] == 0 or A.shape[1] == 0:
+        if not isinstance(seq, RotationSequence):
+            length = A.shape[0] if side is Side.LEFT else A.shape[1]
+            if length < 2:
+                raise ValueError("matrix needs at least 2 columns")
+        return
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    tdt = torch.float64 if A.dtype == np.float64 else torch.float32
+    dA = _np_to_device(A, tdt, dev)
+    apply_device(dA, seq, kind, fast, side, order, algo, workspace)
+    torch.from_numpy(A).copy_(dA.cpu())
+
+
+def apply_naive(A, seq: RotationSequence, kind=TransformKind.ROTATION, fast: bool = False) -> None:
+    """Reference signature (core.py:365-374), executed by the B200 pipeline.
+
+    Result is bit-identical to the reference's strict ``apply_naive`` when
+    ``fast`` is False (every variant in the reference is, SPEC criterion 1)."""
+    apply_cuda(A, seq, kind=kind, fast=fast)
+
+
+def apply_blocked(A, seq: RotationSequence, plan=None, shape=None, kind=TransformKind.ROTATION,
+                  threads: int = 1, fast: bool = False, use_kernel: bool = True) -> None:
+    """Reference signature (blocking.py:420-429). ``plan``/``shape``/``threads``
+    are CPU cache and thread knobs; the GPU tiling is chosen by the library, so
+    they are validated for sign only and otherwise ignored."""
+    if threads < 1:
+        raise ValueError(f"threads must be >= 1, got {threads}")
+    apply_cuda(A, seq, kind=kind, fast=fast)

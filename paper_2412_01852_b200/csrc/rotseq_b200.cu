@@ -1,0 +1,768 @@
+// rotseq_b200.cu — B200-native (sm_100a) application of a rotation sequence to a
+// column-major matrix. C-ABI declared in include/rotseq_b200.h.
+//
+// What the reference does (Python + numba, CPU):
+//   semantic definition  _naive_py            /root/reference/pkg/src/rotseq/core.py:195-205
+//   2x2 formulas         _rot_cols/_refl_cols  core.py:130-149
+//   wavefront schedule   _span_impl            core.py:152-172 (wave t, lane l -> (t-l, p0+l))
+//   hot loop             _kernel_chunk_py      blocking.py:342-397 (startup triangle,
+//                        n_b-wave windows with wave-major coefficient tiles, shutdown triangle)
+//   threads over rows    _run_row_ranges       blocking.py:518-526
+//
+// The B200 design:
+//   * A "unit" is (tile of 32*R owners, band of K consecutive sweeps). One warp runs one
+//     unit: every lane owns R rows (right side; columns for the left side) and keeps a
+//     (K+1)-column window of them in registers. Waves are processed in blocks of K+1 so
+//     the window rotates through fixed registers (slot = column mod (K+1)) — true register
+//     residency, which the reference only models (SURVEY §2 note, kernels.py:135-147).
+//   * Bands of one tile are chained warp-to-warp through shared-memory rings guarded by
+//     mbarriers: warp w streams finished columns of band b to warp w+1 (band b+1), so A
+//     crosses HBM once per chain instead of once per band.
+//   * Coefficients are repacked once per call into a band-major, wave-major stream of
+//     (c,s) pairs (the GPU analogue of the reference's per-window coefficient gather,
+//     blocking.py:364-373) and staged per block by cp.async.bulk (TMA bulk copy) into a
+//     per-warp double buffer; every lane reads them as broadcast LDS.128.
+//   * A persistent grid of one CTA per SM splits the unit list (tile-major) evenly; a
+//     chain that crosses a CTA boundary (or a round boundary inside a CTA) is handed off
+//     through A itself (in place) with per-unit release/acquire progress flags in global
+//     memory. All CTAs are co-resident (cooperative launch), so waits always make progress.
+//   * strict mode uses __dmul_rn/__dadd_rn/__dsub_rn in the reference's exact expression
+//     shape (no contraction => bit-identical to the reference strict build); fast mode uses
+//     2 DMUL + 2 DFMA per rotation element (the 4-instruction minimum for 6 flops).
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "rotseq_b200.h"
+
+#define RS_VERSION 10000
+
+namespace {
+
+// ------------------------------------------------------------------------------------
+// compile-time geometry
+// ------------------------------------------------------------------------------------
+constexpr int kK = 8;          // sweeps per band (lanes of the wavefront)
+constexpr int kR = 1;          // owners (rows) per thread
+constexpr int kStages = 3;     // ring depth in chunks of K+1 columns
+constexpr int kMaxWarps = 24;  // warps per CTA upper bound (launch bounds)
+constexpr int kTileOwners = 32 * kR;
+
+enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
+enum : int { DST_RING = 0, DST_GLOBAL = 1, DST_FLAG = 2 };
+
+std::atomic<long long> g_launches{0};
+thread_local std::string g_err;
+
+rs_status fail(rs_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+// ------------------------------------------------------------------------------------
+// coefficient records and arithmetic
+// ------------------------------------------------------------------------------------
+template <typename T, bool REFL>
+struct Coef;
+template <typename T>
+struct alignas(2 * sizeof(T)) Coef<T, false> {
+  T c, s;
+};
+template <typename T>
+struct alignas(4 * sizeof(T)) Coef<T, true> {
+  T s, d, e, pad;  // d = c - s, e = c + s (hoisted exactly as core.py:142-143)
+};
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+// Rotation (core.py:130-137):   x' = c*x + s*y ; y' = c*y - s*x
+// Reflector (core.py:140-149):  w = s*(x+y) ; x' = w + d*x ; y' = w - e*y
+template <typename T, bool STRICT>
+__device__ __forceinline__ void rot2(T& x, T& y, T c, T s) {
+  if constexpr (STRICT) {
+    const T nx = add_rn(mul_rn(c, x), mul_rn(s, y));
+    const T ny = sub_rn(mul_rn(c, y), mul_rn(s, x));
+    x = nx;
+    y = ny;
+  } else {
+    const T cx = mul_rn(c, x);
+    const T sx = mul_rn(s, x);
+    x = fma_rn(s, y, cx);
+    y = fma_rn(c, y, -sx);
+  }
+}
+template <typename T, bool STRICT>
+__device__ __forceinline__ void refl2(T& x, T& y, T s, T d, T e) {
+  const T w = mul_rn(s, add_rn(x, y));
+  if constexpr (STRICT) {
+    x = add_rn(w, mul_rn(d, x));
+    y = sub_rn(w, mul_rn(e, y));
+  } else {
+    x = fma_rn(d, x, w);
+    y = fma_rn(-e, y, w);
+  }
+}
+template <typename T, bool STRICT, bool REFL>
+__device__ __forceinline__ void xform(T& x, T& y, const Coef<T, REFL>& cf) {
+  if constexpr (REFL) {
+    refl2<T, STRICT>(x, y, cf.s, cf.d, cf.e);
+  } else {
+    rot2<T, STRICT>(x, y, cf.c, cf.s);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// PTX helpers: mbarrier, bulk copy, flags
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "RS_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra RS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// One elected lane: expect `bytes` on `bar` and start a TMA bulk copy global -> shared.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void wait_flag(const uint32_t* p, uint32_t target) {
+  while (ld_acquire(p) < target) __nanosleep(64);
+}
+
+// ------------------------------------------------------------------------------------
+// kernel parameters
+// ------------------------------------------------------------------------------------
+struct PipeParams {
+  void* A;               // element (owner o, wave-column v) at A + o*os + v*cs
+  long long os;          // owner stride (elements)
+  long long cs;          // wave-column stride (elements, negative for reverse order)
+  long long owners;      // independent lines (rows for right side, columns for left)
+  long long units;       // tiles * bands
+  const void* coef;      // packed coefficient stream [bands][nblk][K+1][K]
+  uint32_t* flags;       // [units] chunk-progress flags for in-place hand-offs
+  int len;               // length of the rotated dimension (n right, m left)
+  int k;                 // sweeps
+  int bands;             // ceil(k / K)
+  int nchunk;            // ceil(len / (K+1))
+  int nblk;              // nchunk + 1
+  int nw;                // warps per CTA
+};
+
+// ------------------------------------------------------------------------------------
+// one block of K+1 waves for one warp (fully unrolled; window slots are compile-time)
+//   block b covers waves t = b(K+1)-1 .. b(K+1)+K-1. At the start of wave u it emits
+//   column (b-1)(K+1)+u (finished after wave t-1) from slot u, then loads column
+//   b(K+1)+u into slot u; lane l rotates columns (t-l, t-l+1) = slots (u-1-l, u-l).
+// ------------------------------------------------------------------------------------
+template <typename T, int K, int R, bool STRICT, bool REFL, bool EDGE, bool OUTRING>
+__device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>* __restrict__ cb,
+                                          const T* __restrict__ islot, T* __restrict__ oslot,
+                                          T* const (&gline)[R], const bool (&ok)[R], long long cs,
+                                          int b, int len, int Kb, int lane, bool has_in, bool has_out) {
+  constexpr int TR = 32 * R;
+  const long long c0 = (long long)b * (K + 1);
+#pragma unroll
+  for (int u = 0; u <= K; ++u) {
+    if (has_out) {
+      const long long col = c0 - (K + 1) + u;
+      if (!EDGE || col < len) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (OUTRING) {
+            oslot[u * TR + lane + 32 * r] = w[r][u];
+          } else {
+            if (ok[r]) gline[r][col * cs] = w[r][u];
+          }
+        }
+      }
+    }
+    {
+      const long long col = c0 + u;
+      if (!EDGE || (has_in && col < len)) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[r][u] = islot[u * TR + lane + 32 * r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[r][u] = T(0);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      constexpr int M = K + 1;
+      const int sx = (u - 1 - l + 2 * M) % M;
+      const int sy = (sx + 1) % M;
+      if (EDGE) {
+        const long long j = c0 + u - 1 - l;
+        if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
+      }
+      const Coef<T, REFL> cf = cb[u * K + l];
+#pragma unroll
+      for (int r = 0; r < R; ++r) xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// the persistent band-pipeline kernel
+// ------------------------------------------------------------------------------------
+template <typename T, int K, int R, bool STRICT, bool REFL>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
+  using CoefT = Coef<T, REFL>;
+  constexpr int TR = 32 * R;
+  constexpr int CHUNK = (K + 1) * TR;  // elements of one ring chunk (K+1 columns x TR owners)
+  constexpr int CBLK = (K + 1) * K;    // coefficient records per block
+  constexpr int S = kStages;
+  constexpr int NBAR = 2 * S + 2;      // full[S], empty[S], coef[2] per warp
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NW = P.nw;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);
+  T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * CBLK);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
+
+  if (threadIdx.x < NW) {
+    uint64_t* bw = bars + threadIdx.x * NBAR;
+#pragma unroll
+    for (int i = 0; i < NBAR; ++i) mbar_init(bw + i, 1);
+  }
+  __syncthreads();
+
+  const long long U = P.units;
+  const long long G = gridDim.x;
+  const long long ub = U * (long long)blockIdx.x / G;
+  const long long ue = U * (long long)(blockIdx.x + 1) / G;
+
+  T* const A = reinterpret_cast<T*>(P.A);
+  const int len = P.len;
+  const int nchunk = P.nchunk;
+  const int nblk = P.nblk;
+  uint64_t* const bar_in = bars + warp * NBAR;            // full_in[S], empty_in[S], coef[2]
+  uint64_t* const full_in = bar_in;
+  uint64_t* const empty_in = bar_in + S;
+  uint64_t* const cbar = bar_in + 2 * S;
+  uint64_t* const full_out = bars + (warp + 1) * NBAR;     // next warp's ring (only with DST_RING)
+  uint64_t* const empty_out = full_out + S;
+  T* const rin = ring_sm + (size_t)warp * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
+  CoefT* const cbuf = coef_sm + (size_t)warp * 2 * CBLK;
+  constexpr uint32_t kCoefBytes = (uint32_t)(CBLK * sizeof(CoefT));
+
+  uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
+
+  for (int jr = 0;; ++jr) {
+    const long long u = ub + (long long)jr * NW + warp;
+    if (u >= ue) break;
+    const long long tile = u / P.bands;
+    const int band = (int)(u - tile * P.bands);
+    const int Kb = min(K, P.k - band * K);
+    const int src = band == 0 ? SRC_GLOBAL : ((warp > 0 && u - 1 >= ub) ? SRC_RING : SRC_FLAG);
+    const int dst = band == P.bands - 1 ? DST_GLOBAL : ((warp < NW - 1 && u + 1 < ue) ? DST_RING : DST_FLAG);
+
+    T* gline[R];
+    bool ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long o = tile * TR + lane + 32 * r;
+      ok[r] = o < P.owners;
+      gline[r] = A + (ok[r] ? o : 0) * P.os;
+    }
+    const CoefT* csrc = reinterpret_cast<const CoefT*>(P.coef) + (size_t)band * nblk * CBLK;
+    const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
+    const uint32_t* myflag = P.flags + u;
+
+    // coefficient block 0 of this unit
+    if (lane == 0) bulk_g2s(cbuf + (cseq & 1) * CBLK, csrc, kCoefBytes, &cbar[cseq & 1]);
+
+    // self-filled input (band 0 reads A; a hand-off reads A after the producer's flag)
+    T pre[R][K + 1];
+    auto load_chunk = [&](int q) {
+      if (src == SRC_FLAG) wait_flag(myflag, (uint32_t)q + 1);
+#pragma unroll
+      for (int v = 0; v <= K; ++v) {
+        const long long col = (long long)q * (K + 1) + v;
+#pragma unroll
+        for (int r = 0; r < R; ++r) pre[r][v] = (ok[r] && col < len) ? __ldcg(gline[r] + col * P.cs) : T(0);
+      }
+    };
+    auto produce_self = [&](int q) {
+      const uint32_t seq = seq0 + (uint32_t)q;
+      const uint32_t slot = seq % S;
+      if (seq >= (uint32_t)S) mbar_wait(&empty_in[slot], ((seq / S) & 1u) ^ 1u);
+      T* dstp = rin + slot * CHUNK;
+#pragma unroll
+      for (int v = 0; v <= K; ++v)
+#pragma unroll
+        for (int r = 0; r < R; ++r) dstp[v * TR + lane + 32 * r] = pre[r][v];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_in[slot]);
+    };
+    if (src != SRC_RING) {
+      load_chunk(0);
+      produce_self(0);
+    }
+
+    T w[R][K + 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) w[r][s] = T(0);
+
+    const bool full_band = (Kb == K);
+    const int full_hi = (full_band && len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
+
+    for (int b = 0; b < nblk; ++b) {
+      if (lane == 0 && b + 1 < nblk)
+        bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes,
+                 &cbar[(cseq + 1) & 1]);
+      const bool self_next = (src != SRC_RING) && (b + 1 < nchunk);
+      if (self_next) load_chunk(b + 1);
+
+      mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
+      const bool has_in = b < nchunk;
+      const bool has_out = b >= 1;
+      const uint32_t iseq = seq0 + (uint32_t)b;
+      const T* islot = rin + (iseq % S) * CHUNK;
+      if (has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+      const uint32_t oseq = seq0 + (uint32_t)b - 1u;
+      T* oslot = rout + (oseq % S) * CHUNK;
+      if (dst == DST_RING && has_out && oseq >= (uint32_t)S) mbar_wait(&empty_out[oseq % S], ((oseq / S) & 1u) ^ 1u);
+
+      const CoefT* cb = cbuf + (cseq & 1) * CBLK;
+      const bool interior = b >= 1 && b <= full_hi;
+      if (interior) {
+        if (dst == DST_RING)
+          run_block<T, K, R, STRICT, REFL, false, true>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+                                                        has_in, has_out);
+        else
+          run_block<T, K, R, STRICT, REFL, false, false>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+                                                         has_in, has_out);
+      } else {
+        if (dst == DST_RING)
+          run_block<T, K, R, STRICT, REFL, true, true>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+                                                       has_in, has_out);
+        else
+          run_block<T, K, R, STRICT, REFL, true, false>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+                                                        has_in, has_out);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (has_in) mbar_arrive(&empty_in[iseq % S]);
+        if (dst == DST_RING && has_out) mbar_arrive(&full_out[oseq % S]);
+      }
+      if (dst == DST_FLAG && has_out) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(P.flags + u + 1, (uint32_t)b);
+      }
+      if (self_next) produce_self(b + 1);
+      ++cseq;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// coefficient repack: C/S (len-1) x k column-major -> [bands][nblk][K+1][K] records.
+// Entry (band, b, u, l) holds sweep p = band*K + l, rotation j = b(K+1)+u-1-l, or zeros
+// when that lane is idle (startup/shutdown triangles, partial last band). Reverse order
+// mirrors j and negates S (rotation) or C (reflector): both exact in IEEE arithmetic.
+// ------------------------------------------------------------------------------------
+template <typename T, int K, bool REFL>
+__global__ void rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C, const T* __restrict__ Sm,
+                               long long ldcs, int len, int k, int bands, int nblk, int rev) {
+  const long long total = (long long)bands * nblk * (K + 1) * K;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(e % K);
+    long long r = e / K;
+    const int u = (int)(r % (K + 1));
+    r /= (K + 1);
+    const long long b = r % nblk;
+    const int band = (int)(r / nblk);
+    const int p = band * K + l;
+    const long long j = b * (K + 1) + u - 1 - l;
+    Coef<T, REFL> cf;
+    if (p < k && j >= 0 && j <= (long long)len - 2) {
+      const long long jj = rev ? (long long)len - 2 - j : j;
+      T c = C[jj + (long long)p * ldcs];
+      T s = Sm[jj + (long long)p * ldcs];
+      if constexpr (REFL) {
+        if (rev) c = -c;
+        cf.s = s;
+        cf.d = c - s;
+        cf.e = c + s;
+        cf.pad = T(0);
+      } else {
+        if (rev) s = -s;
+        cf.c = c;
+        cf.s = s;
+      }
+    } else {
+      if constexpr (REFL) {
+        cf.s = T(0);
+        cf.d = T(0);
+        cf.e = T(0);
+        cf.pad = T(0);
+      } else {
+        cf.c = T(0);
+        cf.s = T(0);
+      }
+    }
+    out[e] = cf;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// naive kernel: one thread per owner, plain sweep loop (GPU restatement of _naive_py,
+// core.py:195-205); independent second implementation used for cross-checks.
+// ------------------------------------------------------------------------------------
+template <typename T, bool STRICT, bool REFL>
+__global__ void rs_naive_kernel(T* __restrict__ A, long long os, long long cs, long long owners, int len,
+                                const T* __restrict__ C, const T* __restrict__ Sm, long long ldcs, int k, int rev) {
+  const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (o >= owners) return;
+  T* a = A + o * os;
+  for (int p = 0; p < k; ++p) {
+    for (int jj = 0; jj < len - 1; ++jj) {
+      const long long j = rev ? (long long)len - 2 - jj : jj;
+      const T c = C[j + (long long)p * ldcs];
+      const T s = Sm[j + (long long)p * ldcs];
+      T x = a[j * cs];
+      T y = a[(j + 1) * cs];
+      if constexpr (REFL) {
+        const T d = sub_rn(c, s);
+        const T e = add_rn(c, s);
+        refl2<T, STRICT>(x, y, s, d, e);
+      } else {
+        rot2<T, STRICT>(x, y, c, s);
+      }
+      a[j * cs] = x;
+      a[(j + 1) * cs] = y;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+struct Geometry {
+  long long owners = 0;
+  int len = 0;
+  long long os = 0, cs = 0;
+  int k = 0;
+  int bands = 0;
+  long long tiles = 0;
+  long long units = 0;
+  int nchunk = 0;
+  int nblk = 0;
+  size_t coef_bytes = 0;
+  size_t flag_bytes = 0;
+  size_t coef_rec = 0;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int kind, int dtype, Geometry* g) {
+  const bool left = side == RS_SIDE_LEFT;
+  g->owners = left ? n : m;
+  g->len = (int)(left ? m : n);
+  g->os = left ? lda : 1;
+  g->cs = left ? 1 : lda;
+  g->k = (int)k;
+  g->bands = (int)((k + kK - 1) / kK);
+  g->tiles = (g->owners + kTileOwners - 1) / kTileOwners;
+  g->units = g->tiles * g->bands;
+  g->nchunk = (g->len + kK) / (kK + 1);
+  g->nblk = g->nchunk + 1;
+  const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
+  g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 : 2) * tsz;
+  g->coef_bytes = align_up((size_t)g->bands * g->nblk * (kK + 1) * kK * g->coef_rec, 256);
+  g->flag_bytes = align_up((size_t)(g->units + 1) * sizeof(uint32_t), 256);
+  return true;
+}
+
+struct LaunchPlan {
+  int grid = 0;
+  int nw = 0;
+  size_t smem = 0;
+};
+
+size_t smem_per_warp(size_t tsz, size_t coef_rec) {
+  return 2 * (size_t)(kK + 1) * kK * coef_rec + (size_t)kStages * (kK + 1) * kTileOwners * tsz +
+         (2 * kStages + 2) * sizeof(uint64_t);
+}
+
+rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ECUDA, "cudaGetDevice failed");
+  int sms = 0, optin = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
+  const size_t per = smem_per_warp(tsz, g.coef_rec);
+  // one extra barrier block for the (never used) ring of warp nw
+  int cap = (int)((optin - (2 * kStages + 2) * sizeof(uint64_t)) / per);
+  if (cap > kMaxWarps) cap = kMaxWarps;
+  if (cap < 1) return fail(RS_EUNSUPPORTED, "shared memory too small for one pipeline warp");
+  long long grid = sms;
+  if (g.units < grid) grid = g.units;
+  if (grid < 1) grid = 1;
+  const double x = (double)g.units / (double)grid;
+  // units per CTA x: one round of ceil(x) warps when it fits, else the fewest rounds of
+  // at most `cap` warps, spread evenly so the last round is as full as possible.
+  long long rounds = (long long)ceil(x / cap);
+  if (rounds < 1) rounds = 1;
+  int nw = (int)ceil(x / (double)rounds);
+  if (nw > cap) nw = cap;
+  if (nw < 1) nw = 1;
+  lp->grid = (int)grid;
+  lp->nw = nw;
+  lp->smem = per * nw + (2 * kStages + 2) * sizeof(uint64_t);
+  return RS_OK;
+}
+
+template <typename T, bool STRICT, bool REFL>
+rs_status launch_pipeline(const Geometry& g, T* Abase, const T* C, const T* S, long long ldcs, int rev,
+                          void* ws, cudaStream_t st) {
+  using CoefT = Coef<T, REFL>;
+  LaunchPlan lp;
+  rs_status rc = plan_launch(g, sizeof(T), &lp);
+  if (rc != RS_OK) return rc;
+  CoefT* coef = reinterpret_cast<CoefT*>(ws);
+  uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes);
+  cudaError_t e = cudaMemsetAsync(flags, 0, g.flag_bytes, st);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
+  {
+    const long long total = (long long)g.bands * g.nblk * (kK + 1) * kK;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    if (blocks < 1) blocks = 1;
+    rs_pack_kernel<T, kK, REFL><<<(unsigned)blocks, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.bands, g.nblk, rev);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
+  }
+  PipeParams P;
+  P.A = Abase;
+  P.os = g.os;
+  P.cs = rev ? -g.cs : g.cs;
+  if (rev) P.A = Abase + (long long)(g.len - 1) * g.cs;
+  P.owners = g.owners;
+  P.units = g.units;
+  P.coef = coef;
+  P.flags = flags;
+  P.len = g.len;
+  P.k = g.k;
+  P.bands = g.bands;
+  P.nchunk = g.nchunk;
+  P.nblk = g.nblk;
+  P.nw = lp.nw;
+  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL>;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp.smem);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)lp.grid);
+  cfg.blockDim = dim3((unsigned)(lp.nw * 32));
+  cfg.dynamicSmemBytes = lp.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, P);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pipeline launch: ") + cudaGetErrorString(e));
+  return RS_OK;
+}
+
+template <typename T, bool STRICT, bool REFL>
+rs_status launch_naive(const Geometry& g, T* A, const T* C, const T* S, long long ldcs, int rev, cudaStream_t st) {
+  const long long blocks = (g.owners + 127) / 128;
+  rs_naive_kernel<T, STRICT, REFL><<<(unsigned)blocks, 128, 0, st>>>(A, g.os, g.cs, g.owners, g.len, C, S, ldcs,
+                                                                       g.k, rev);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("naive launch: ") + cudaGetErrorString(e));
+  return RS_OK;
+}
+
+template <typename T>
+rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs,
+                     int64_t k, int side, int order, int kind, int strict, void* workspace, size_t ws_bytes,
+                     void* stream) {
+  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+  if (side != RS_SIDE_RIGHT && side != RS_SIDE_LEFT) return fail(RS_EINVAL, "side must be 0 (right) or 1 (left)");
+  if (order != RS_ORDER_FORWARD && order != RS_ORDER_REVERSE)
+    return fail(RS_EINVAL, "order must be 0 (forward) or 1 (reverse)");
+  if (kind != RS_KIND_ROTATION && kind != RS_KIND_REFLECTOR)
+    return fail(RS_EINVAL, "kind must be 0 (rotation) or 1 (reflector)");
+  if (algo != RS_ALGO_PIPELINE && algo != RS_ALGO_NAIVE) return fail(RS_EINVAL, "unknown algorithm");
+  if (m < 0 || n < 0) return fail(RS_EINVAL, "matrix dimensions must be non-negative");
+  const bool left = side == RS_SIDE_LEFT;
+  const int64_t len = left ? m : n;
+  const int64_t owners = left ? n : m;
+  if (len < 2)
+    return fail(RS_EINVAL, left ? "matrix needs at least 2 rows for left-side application"
+                                : "matrix needs at least 2 columns");
+  if (len > (int64_t)1 << 30) return fail(RS_EUNSUPPORTED, "rotated dimension too long");
+  if (k < 1) return fail(RS_EINVAL, "need k >= 1 sequences");
+  if (k > (int64_t)1 << 24) return fail(RS_EUNSUPPORTED, "too many sequences");
+  if (lda < (m > 1 ? m : 1)) return fail(RS_EINVAL, "lda must be >= max(1, m) (column-major)");
+  if (ldcs < len - 1) return fail(RS_EINVAL, "ldcs must be >= len - 1");
+  if (owners == 0) return RS_OK;  // no rows: no-op (blocking.py:446-447)
+  if (!A || !C || !S) return fail(RS_EINVAL, "null pointer");
+  Geometry g;
+  make_geometry(m, n, lda, k, side, kind, dtype, &g);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int rev = order == RS_ORDER_REVERSE;
+  if (algo == RS_ALGO_NAIVE) {
+    if (strict) {
+      return kind == RS_KIND_REFLECTOR ? launch_naive<T, true, true>(g, A, C, S, ldcs, rev, st)
+                                       : launch_naive<T, true, false>(g, A, C, S, ldcs, rev, st);
+    }
+    return kind == RS_KIND_REFLECTOR ? launch_naive<T, false, true>(g, A, C, S, ldcs, rev, st)
+                                     : launch_naive<T, false, false>(g, A, C, S, ldcs, rev, st);
+  }
+  const size_t need = g.coef_bytes + g.flag_bytes;
+  void* ws = workspace;
+  bool owned = false;
+  if (ws == nullptr) {
+    cudaError_t e = cudaMallocAsync(&ws, need, st);
+    if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    owned = true;
+  } else if (ws_bytes < need) {
+    return fail(RS_ENOMEM, "workspace smaller than rs_workspace_bytes()");
+  } else if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) {
+    return fail(RS_EINVAL, "workspace must be 256-byte aligned");
+  }
+  rs_status rc;
+  if (strict) {
+    rc = kind == RS_KIND_REFLECTOR ? launch_pipeline<T, true, true>(g, A, C, S, ldcs, rev, ws, st)
+                                   : launch_pipeline<T, true, false>(g, A, C, S, ldcs, rev, ws, st);
+  } else {
+    rc = kind == RS_KIND_REFLECTOR ? launch_pipeline<T, false, true>(g, A, C, S, ldcs, rev, ws, st)
+                                   : launch_pipeline<T, false, false>(g, A, C, S, ldcs, rev, ws, st);
+  }
+  if (owned) {
+    cudaError_t e = cudaFreeAsync(ws, st);
+    if (rc == RS_OK && e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFreeAsync: ") + cudaGetErrorString(e));
+  }
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rs_version(void) { return RS_VERSION; }
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+size_t rs_workspace_bytes(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype) {
+  if (m < 0 || n < 0 || k < 1) return 0;
+  if (side != RS_SIDE_RIGHT && side != RS_SIDE_LEFT) return 0;
+  if (kind != RS_KIND_ROTATION && kind != RS_KIND_REFLECTOR) return 0;
+  if (dtype != RS_DTYPE_F64 && dtype != RS_DTYPE_F32) return 0;
+  const int64_t len = side == RS_SIDE_LEFT ? m : n;
+  if (len < 2) return 0;
+  Geometry g;
+  make_geometry(m, n, m > 1 ? m : 1, k, side, kind, dtype, &g);
+  return g.coef_bytes + g.flag_bytes;
+}
+
+rs_status rs_apply_f64(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S, int64_t ldcs,
+                       int64_t k, int side, int order, int kind, int strict, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  g_err.clear();
+  return apply_impl<double>(RS_ALGO_PIPELINE, A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, workspace,
+                            workspace_bytes, stream);
+}
+
+rs_status rs_apply_f32(float* A, int64_t m, int64_t n, int64_t lda, const float* C, const float* S, int64_t ldcs,
+                       int64_t k, int side, int order, int kind, int strict, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  g_err.clear();
+  return apply_impl<float>(RS_ALGO_PIPELINE, A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, workspace,
+                           workspace_bytes, stream);
+}
+
+rs_status rs_apply_algo_f64(int algo, double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S,
+                            int64_t ldcs, int64_t k, int side, int order, int kind, int strict, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return apply_impl<double>(algo, A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, workspace,
+                            workspace_bytes, stream);
+}
+
+rs_status rs_apply_algo_f32(int algo, float* A, int64_t m, int64_t n, int64_t lda, const float* C, const float* S,
+                            int64_t ldcs, int64_t k, int side, int order, int kind, int strict, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return apply_impl<float>(algo, A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, workspace,
+                           workspace_bytes, stream);
+}
+
+rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype, int* grid_ctas,
+                       int* warps_per_cta, int64_t* units, int* band_width, int* rows_per_tile, size_t* smem_bytes) {
+  g_err.clear();
+  if (m < 0 || n < 0 || k < 1) return fail(RS_EINVAL, "bad dimensions");
+  const int64_t len = side == RS_SIDE_LEFT ? m : n;
+  if (len < 2) return fail(RS_EINVAL, "rotated dimension must be >= 2");
+  Geometry g;
+  make_geometry(m, n, m > 1 ? m : 1, k, side, kind, dtype, &g);
+  LaunchPlan lp;
+  rs_status rc = plan_launch(g, dtype == RS_DTYPE_F64 ? 8 : 4, &lp);
+  if (rc != RS_OK) return rc;
+  if (grid_ctas) *grid_ctas = lp.grid;
+  if (warps_per_cta) *warps_per_cta = lp.nw;
+  if (units) *units = g.units;
+  if (band_width) *band_width = kK;
+  if (rows_per_tile) *rows_per_tile = kTileOwners;
+  if (smem_bytes) *smem_bytes = lp.smem;
+  return RS_OK;
+}
+
+int64_t rs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// Steady-state inner-loop ceiling: register window of K+1 cols x R rows per thread,
+// (c,s) pairs from smem (LDS.128 broadcast), column in/out from smem. No HBM traffic.
+#include <cstdio>
+#include <cuda_runtime.h>
+template <int K, int R, bool STRICT>
+__global__ void steady(double* out, int nblocks, int cw) {
+  extern __shared__ double2 sm[];
+  double2* coef = sm;                        // [cw][K] per block
+  double* io = (double*)(sm + cw * K);       // per warp 32*R doubles x (K+1)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < cw * K; i += blockDim.x) {
+    double th = 0.001 * i; coef[i] = make_double2(cos(th), sin(th));
+  }
+  double* myio = io + warp * 32 * R * (K + 1);
+  for (int i = lane; i < 32 * R * (K + 1); i += 32) myio[i] = 1.0 + i;
+  __syncthreads();
+  double w[R][K + 1];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int s = 0; s <= K; ++s) w[r][s] = 0.5 * s + r;
+  int cbase = 0;
+  for (int b = 0; b < nblocks; ++b) {
+#pragma unroll
+    for (int u = 0; u < K + 1; ++u) {
+      const int sin_ = (u + 1) % (K + 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) w[r][sin_] = myio[(u * R + r) * 32 + lane];
+#pragma unroll
+      for (int l = 0; l < K; ++l) {
+        const double2 cs = coef[cbase + u * K + l];
+        const int sx = ((u - l) % (K + 1) + (K + 1)) % (K + 1);
+        const int sy = (sx + 1) % (K + 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double x = w[r][sx], y = w[r][sy];
+          if (STRICT) {
+            w[r][sx] = __dadd_rn(__dmul_rn(cs.x, x), __dmul_rn(cs.y, y));
+            w[r][sy] = __dsub_rn(__dmul_rn(cs.x, y), __dmul_rn(cs.y, x));
+          } else {
+            const double cx = cs.x * x, sxx = cs.y * x;
+            w[r][sx] = fma(cs.y, y, cx);
+            w[r][sy] = fma(cs.x, y, -sxx);
+          }
+        }
+      }
+      const int sout = ((u - K + 1) % (K + 1) + (K + 1)) % (K + 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) myio[(u * R + r) * 32 + lane] = w[r][sout];
+    }
+    cbase += (K + 1) * K;
+    if (cbase + (K + 1) * K > cw * K) cbase = 0;
+  }
+  double s = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int q = 0; q <= K; ++q) s += w[r][q];
+  if (s == 1.2345) out[0] = s;
+}
+template <int K, int R, bool STRICT>
+void run(int warps_per_cta, int ctas_per_sm) {
+  int cw = 64 * (K + 1);
+  size_t smem = cw * K * 16 + (size_t)warps_per_cta * 32 * R * (K + 1) * 8;
+  cudaFuncSetAttribute(steady<K, R, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  double* o; cudaMalloc(&o, 8);
+  int grid = 148 * ctas_per_sm, nb = 2000 / (K + 1) * 4;
+  steady<K, R, STRICT><<<grid, warps_per_cta * 32, smem>>>(o, nb, cw);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  steady<K, R, STRICT><<<grid, warps_per_cta * 32, smem>>>(o, nb, cw);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  double fl = 6.0 * (double)grid * warps_per_cta * 32 * R * (double)nb * (K + 1) * K;
+  printf("K=%2d R=%d strict=%d warps/SM=%2d: %.2f TF/s (%.1f%% of 34.2)  %s\n", K, R, STRICT,
+         warps_per_cta * ctas_per_sm, fl / ms / 1e9, fl / ms / 1e9 / 34.2 * 100, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(o);
+}
+int main() {
+  run<8, 1, false>(8, 1); run<8, 1, false>(16, 1); run<8, 1, false>(24, 1); run<8, 1, false>(32, 1);
+  run<8, 2, false>(8, 1); run<8, 2, false>(12, 1); run<8, 2, false>(16, 1); run<8, 2, false>(24, 1);
+  run<4, 2, false>(16, 1); run<6, 2, false>(16, 1); run<12, 1, false>(16, 1); run<16, 1, false>(16, 1);
+  run<8, 4, false>(8, 1); run<8, 4, false>(12, 1);
+  run<8, 1, true>(16, 1); run<8, 2, true>(16, 1); run<8, 2, true>(24, 1);
+  return 0;
+}
