@@ -40,6 +40,7 @@ EXPORTS = (
     "rs_apply_algo_f32",
     "rs_plan_info",
     "rs_launch_count",
+    "rs_debug_set_trace",
 )
 
 _lock = threading.Lock()
@@ -73,6 +74,8 @@ def _declare(lib):
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(sz)]
     lib.rs_launch_count.restype = i64
     lib.rs_launch_count.argtypes = []
+    lib.rs_debug_set_trace.restype = i32
+    lib.rs_debug_set_trace.argtypes = [vp]
     return lib
 
 

@@ -46,7 +46,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         return OUT
     fd, tmp = tempfile.mkstemp(suffix=".so", dir=HERE)
     os.close(fd)
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
+    extra = os.environ.get("RS_NVCC_EXTRA", "").split()
+    cmd = [nvcc_path(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         os.unlink(tmp)

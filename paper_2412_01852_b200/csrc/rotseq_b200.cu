@@ -36,6 +36,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -49,10 +50,11 @@ namespace {
 // compile-time geometry
 // ------------------------------------------------------------------------------------
 constexpr int kK = 8;          // sweeps per band (lanes of the wavefront)
-constexpr int kR = 1;          // owners (rows) per thread
+constexpr int kR = 2;          // owners (rows) per thread
 constexpr int kStages = 3;     // ring depth in chunks of K+1 columns
-constexpr int kMaxWarps = 24;  // warps per CTA upper bound (launch bounds)
+constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
 constexpr int kTileOwners = 32 * kR;
+constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
 
 enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
 enum : int { DST_RING = 0, DST_GLOBAL = 1, DST_FLAG = 2 };
@@ -156,6 +158,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// cp.async (LDGSTS) of one element; src_size 0 zero-fills (out-of-range rows/columns).
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool valid) {
+  if constexpr (sizeof(T) == 8) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -164,8 +181,38 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
+  while (ld_acquire_shared(p) < target) __nanosleep(32);
+}
 __device__ __forceinline__ void wait_flag(const uint32_t* p, uint32_t target) {
   while (ld_acquire(p) < target) __nanosleep(64);
+}
+
+// Debug-only progress trace (rs_debug_set_trace): one 64-bit word per (CTA, warp),
+// (round << 48) | (block << 24) | (state << 16) | position, written to mapped host memory
+// so a stalled launch can be inspected from the host while it runs. Null in production.
+// Compiled in only with -DRS_TRACE (RS_NVCC_EXTRA=-DRS_TRACE python -m paper_2412_01852_b200.build).
+__device__ unsigned long long* g_trace = nullptr;
+__device__ __forceinline__ void trace(int warp, int jr, int b, int state, long long pos) {
+#ifndef RS_TRACE
+  (void)warp, (void)jr, (void)b, (void)state, (void)pos;
+#else
+  unsigned long long* t = g_trace;
+  if (t != nullptr && (threadIdx.x & 31) == 0) {
+    const unsigned long long v = ((unsigned long long)(jr & 0xffff) << 48) |
+                                 ((unsigned long long)(b & 0xffffff) << 24) |
+                                 ((unsigned long long)(state & 0xff) << 16) | (unsigned long long)(pos & 0xffff);
+    *(volatile unsigned long long*)(t + (size_t)blockIdx.x * kMaxWarps + warp) = v;
+  }
+#endif
 }
 
 // ------------------------------------------------------------------------------------
@@ -251,7 +298,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   constexpr int CHUNK = (K + 1) * TR;  // elements of one ring chunk (K+1 columns x TR owners)
   constexpr int CBLK = (K + 1) * K;    // coefficient records per block
   constexpr int S = kStages;
-  constexpr int NBAR = 2 * S + 2;      // full[S], empty[S], coef[2] per warp
+  // per-warp control words: full[S] (mbarriers), consumed-chunk counter, coef[2] (mbarriers).
+  // "full" is alias-safe as an mbarrier (the consumer has always seen chunk seq-S before it
+  // waits for seq). "empty" is a monotonic counter instead: a ring's producer changes
+  // between rounds (previous warp vs. self-fill), so a producer may have to wait on a
+  // consumer many phases behind, which a parity test cannot express.
+  constexpr int NBAR = kCtlWords;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
@@ -264,7 +316,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   if (threadIdx.x < NW) {
     uint64_t* bw = bars + threadIdx.x * NBAR;
 #pragma unroll
-    for (int i = 0; i < NBAR; ++i) mbar_init(bw + i, 1);
+    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
+    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
+    mbar_init(bw + S + 1, 1);
+    mbar_init(bw + S + 2, 1);
   }
   __syncthreads();
 
@@ -277,27 +332,47 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   const int len = P.len;
   const int nchunk = P.nchunk;
   const int nblk = P.nblk;
-  uint64_t* const bar_in = bars + warp * NBAR;            // full_in[S], empty_in[S], coef[2]
+  uint64_t* const bar_in = bars + warp * NBAR;             // full_in[S], consumed, coef[2]
   uint64_t* const full_in = bar_in;
-  uint64_t* const empty_in = bar_in + S;
-  uint64_t* const cbar = bar_in + 2 * S;
-  uint64_t* const full_out = bars + (warp + 1) * NBAR;     // next warp's ring (only with DST_RING)
-  uint64_t* const empty_out = full_out + S;
+  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
+  uint64_t* const cbar = bar_in + S + 1;
+  uint64_t* const full_out = bars + (warp + 1) * NBAR;      // next warp's ring (only with DST_RING)
+  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
   CoefT* const cbuf = coef_sm + (size_t)warp * 2 * CBLK;
   constexpr uint32_t kCoefBytes = (uint32_t)(CBLK * sizeof(CoefT));
 
+  // Processing order inside the CTA: when the range ends in a partial tile (its low bands
+  // feed the next CTA), run that tail first so the next CTA's start never waits for this
+  // CTA's last round; the rest follows in natural tile-major order.
+  const int bands = P.bands;
+  const long long tail_start = (ue / bands) * bands;
+  const bool reorder = (ue % bands != 0) && (tail_start > ub);
+  const long long ntail = reorder ? ue - tail_start : 0;
+  auto unit_at = [&](long long p) -> long long {
+    return reorder ? (p < ntail ? tail_start + p : ub + (p - ntail)) : ub + p;
+  };
+  auto pos_of = [&](long long uu) -> long long {
+    return reorder ? (uu >= tail_start ? uu - tail_start : uu - ub + ntail) : uu - ub;
+  };
+
   uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
 
   for (int jr = 0;; ++jr) {
-    const long long u = ub + (long long)jr * NW + warp;
-    if (u >= ue) break;
-    const long long tile = u / P.bands;
-    const int band = (int)(u - tile * P.bands);
+    const long long p = (long long)jr * NW + warp;
+    if (p >= ue - ub) break;
+    const long long u = unit_at(p);
+    const long long tile = u / bands;
+    const int band = (int)(u - tile * bands);
     const int Kb = min(K, P.k - band * K);
-    const int src = band == 0 ? SRC_GLOBAL : ((warp > 0 && u - 1 >= ub) ? SRC_RING : SRC_FLAG);
-    const int dst = band == P.bands - 1 ? DST_GLOBAL : ((warp < NW - 1 && u + 1 < ue) ? DST_RING : DST_FLAG);
+    // producer of u is u-1, consumer is u+1 (same tile); ring hand-off only when they are
+    // adjacent positions of the same round of this CTA, else through A + progress flag.
+    const int src = band == 0 ? SRC_GLOBAL
+                              : ((warp > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
+    const int dst = band == bands - 1
+                        ? DST_GLOBAL
+                        : ((warp < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
 
     T* gline[R];
     bool ok[R];
@@ -314,32 +389,31 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     // coefficient block 0 of this unit
     if (lane == 0) bulk_g2s(cbuf + (cseq & 1) * CBLK, csrc, kCoefBytes, &cbar[cseq & 1]);
 
-    // self-filled input (band 0 reads A; a hand-off reads A after the producer's flag)
-    T pre[R][K + 1];
-    auto load_chunk = [&](int q) {
+    // self-filled input (band 0 reads A; a hand-off reads A after the producer's flag):
+    // cp.async (LDGSTS) straight into this warp's own ring slot, no staging registers.
+    // The slot of chunk q was last used by chunk q-S, consumed by this warp already.
+    auto fill_chunk = [&](int q) {
       if (src == SRC_FLAG) wait_flag(myflag, (uint32_t)q + 1);
+      T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
 #pragma unroll
       for (int v = 0; v <= K; ++v) {
         const long long col = (long long)q * (K + 1) + v;
+        const bool cv = col < len;
 #pragma unroll
-        for (int r = 0; r < R; ++r) pre[r][v] = (ok[r] && col < len) ? __ldcg(gline[r] + col * P.cs) : T(0);
+        for (int r = 0; r < R; ++r)
+          cp_async_elem(dstp + v * TR + lane + 32 * r, gline[r] + (cv ? col * P.cs : 0), ok[r] && cv);
       }
+      cp_async_commit();
     };
-    auto produce_self = [&](int q) {
-      const uint32_t seq = seq0 + (uint32_t)q;
-      const uint32_t slot = seq % S;
-      if (seq >= (uint32_t)S) mbar_wait(&empty_in[slot], ((seq / S) & 1u) ^ 1u);
-      T* dstp = rin + slot * CHUNK;
-#pragma unroll
-      for (int v = 0; v <= K; ++v)
-#pragma unroll
-        for (int r = 0; r < R; ++r) dstp[v * TR + lane + 32 * r] = pre[r][v];
+    auto publish_chunk = [&](int q) {
+      cp_async_wait_all();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_in[slot]);
+      if (lane == 0) mbar_arrive(&full_in[(seq0 + (uint32_t)q) % S]);
     };
+    trace(warp, jr, 0, 1, p);
     if (src != SRC_RING) {
-      load_chunk(0);
-      produce_self(0);
+      fill_chunk(0);
+      publish_chunk(0);
     }
 
     T w[R][K + 1];
@@ -356,18 +430,23 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
         bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes,
                  &cbar[(cseq + 1) & 1]);
       const bool self_next = (src != SRC_RING) && (b + 1 < nchunk);
-      if (self_next) load_chunk(b + 1);
+      trace(warp, jr, b, 2, p);
+      if (self_next) fill_chunk(b + 1);
+      trace(warp, jr, b, 3, p);
 
       mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
       const bool has_in = b < nchunk;
       const bool has_out = b >= 1;
       const uint32_t iseq = seq0 + (uint32_t)b;
       const T* islot = rin + (iseq % S) * CHUNK;
+      trace(warp, jr, b, 4, p);
       if (has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+      trace(warp, jr, b, 5, p);
       const uint32_t oseq = seq0 + (uint32_t)b - 1u;
       T* oslot = rout + (oseq % S) * CHUNK;
-      if (dst == DST_RING && has_out && oseq >= (uint32_t)S) mbar_wait(&empty_out[oseq % S], ((oseq / S) & 1u) ^ 1u);
+      if (dst == DST_RING && has_out && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
 
+      trace(warp, jr, b, 6, p);
       const CoefT* cb = cbuf + (cseq & 1) * CBLK;
       const bool interior = b >= 1 && b <= full_hi;
       if (interior) {
@@ -387,7 +466,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       }
       __syncwarp();
       if (lane == 0) {
-        if (has_in) mbar_arrive(&empty_in[iseq % S]);
+        if (has_in) st_release_shared(consumed_in, iseq + 1u);
         if (dst == DST_RING && has_out) mbar_arrive(&full_out[oseq % S]);
       }
       if (dst == DST_FLAG && has_out) {
@@ -395,10 +474,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
         __syncwarp();
         if (lane == 0) st_release(P.flags + u + 1, (uint32_t)b);
       }
-      if (self_next) produce_self(b + 1);
+      if (self_next) publish_chunk(b + 1);
       ++cseq;
     }
   }
+  trace(warp, 0xffff, 0, 9, 0);
 }
 
 // ------------------------------------------------------------------------------------
@@ -529,7 +609,7 @@ struct LaunchPlan {
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec) {
   return 2 * (size_t)(kK + 1) * kK * coef_rec + (size_t)kStages * (kK + 1) * kTileOwners * tsz +
-         (2 * kStages + 2) * sizeof(uint64_t);
+         kCtlWords * sizeof(uint64_t);
 }
 
 rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
@@ -541,10 +621,19 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
   const size_t per = smem_per_warp(tsz, g.coef_rec);
   // one extra barrier block for the (never used) ring of warp nw
-  int cap = (int)((optin - (2 * kStages + 2) * sizeof(uint64_t)) / per);
+  int cap = (int)((optin - kCtlWords * sizeof(uint64_t)) / per);
   if (cap > kMaxWarps) cap = kMaxWarps;
   if (cap < 1) return fail(RS_EUNSUPPORTED, "shared memory too small for one pipeline warp");
   long long grid = sms;
+  // test hooks: force multi-round / multi-CTA geometry on small problems
+  if (const char* ev = getenv("RS_DEBUG_MAX_WARPS")) {
+    const int v = atoi(ev);
+    if (v >= 1 && v < cap) cap = v;
+  }
+  if (const char* ev = getenv("RS_DEBUG_GRID")) {
+    const long long v = atoll(ev);
+    if (v >= 1 && v < grid) grid = v;
+  }
   if (g.units < grid) grid = g.units;
   if (grid < 1) grid = 1;
   const double x = (double)g.units / (double)grid;
@@ -557,7 +646,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   if (nw < 1) nw = 1;
   lp->grid = (int)grid;
   lp->nw = nw;
-  lp->smem = per * nw + (2 * kStages + 2) * sizeof(uint64_t);
+  lp->smem = per * nw + kCtlWords * sizeof(uint64_t);
   return RS_OK;
 }
 
@@ -764,5 +853,17 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
 }
 
 int64_t rs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+rs_status rs_debug_set_trace(void* device_ptr) {
+  g_err.clear();
+#ifndef RS_TRACE
+  (void)device_ptr;
+  return fail(RS_EUNSUPPORTED, "library built without -DRS_TRACE");
+#endif
+  unsigned long long* p = reinterpret_cast<unsigned long long*>(device_ptr);
+  cudaError_t e = cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("rs_debug_set_trace: ") + cudaGetErrorString(e));
+  return RS_OK;
+}
 
 }  // extern "C"

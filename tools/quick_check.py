@@ -29,4 +29,15 @@ for side in ("right", "left"):
             ok &= run(65, 70, 17, side=side, order=order, kind=kind)
             ok &= run(65, 70, 17, side=side, order=order, kind=kind, fast=True)
 ok &= run(4096, 512, 64)
+# forced multi-round / multi-CTA geometries (exercise ring, flag and reorder paths)
+for mw, grid in [("1", "1"), ("2", "3"), ("3", "2"), ("4", "5"), ("5", "7"), ("2", "")]:
+    os.environ["RS_DEBUG_MAX_WARPS"] = mw
+    if grid: os.environ["RS_DEBUG_GRID"] = grid
+    else: os.environ.pop("RS_DEBUG_GRID", None)
+    print("RS_DEBUG_MAX_WARPS", mw, "RS_DEBUG_GRID", grid)
+    for (m, n, k) in [(100, 50, 40), (300, 37, 33), (64, 200, 70), (33, 9, 24)]:
+        ok &= run(m, n, k)
+    ok &= run(90, 60, 41, side="left", order="reverse", kind="reflector")
+os.environ.pop("RS_DEBUG_MAX_WARPS", None); os.environ.pop("RS_DEBUG_GRID", None)
+ok &= run(65536 // 8, 2048, 256)
 print("ALL OK" if ok else "FAILURES")
