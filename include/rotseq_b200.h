@@ -111,9 +111,10 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
  * process start (all threads). Used by bench.py to report gpu_launches. */
 int64_t rs_launch_count(void);
 
-/* Debug only: install (non-NULL) or remove (NULL) a device-visible buffer of
- * 148*16 uint64 words that the pipeline kernel fills with per-warp progress
- * (round<<48 | block<<24 | state<<16 | position) for post-mortem of stalls. */
+/* Debug only (library built with -DRS_TRACE, else RS_EUNSUPPORTED): install (non-NULL)
+ * or remove (NULL) a device-visible buffer of grid*16*32*10 uint64 words that the
+ * pipeline kernel fills with one record per unit (start/end time, wait/compute cycle
+ * breakdown) for timeline analysis. */
 rs_status rs_debug_set_trace(void* device_ptr);
 
 #ifdef __cplusplus

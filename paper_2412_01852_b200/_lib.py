@@ -13,7 +13,7 @@ import os
 import threading
 
 LIB_NAME = "librotseq_b200.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("RS_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
 
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ENOMEM, RS_EUNSUPPORTED = 0, 1, 2, 3, 4
 STATUS_NAMES = {

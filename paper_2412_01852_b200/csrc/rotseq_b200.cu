@@ -51,10 +51,15 @@ namespace {
 // ------------------------------------------------------------------------------------
 constexpr int kK = 8;          // sweeps per band (lanes of the wavefront)
 constexpr int kR = 2;          // owners (rows) per thread
-constexpr int kStages = 3;     // ring depth in chunks of K+1 columns
+#ifndef RS_STAGES
+#define RS_STAGES 3
+#endif
+constexpr int kStages = RS_STAGES;  // ring depth in chunks of K+1 columns
 constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
 constexpr int kTileOwners = 32 * kR;
 constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
+constexpr int kFlagEvery = 4;   // hand-off progress is published every 4 blocks (fence cost)
+constexpr size_t kTrashBytes = 32 * kR * 8;  // scratch slot per lane for rows past the matrix
 
 enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
 enum : int { DST_RING = 0, DST_GLOBAL = 1, DST_FLAG = 2 };
@@ -192,26 +197,56 @@ __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
 __device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
   while (ld_acquire_shared(p) < target) __nanosleep(32);
 }
-__device__ __forceinline__ void wait_flag(const uint32_t* p, uint32_t target) {
-  while (ld_acquire(p) < target) __nanosleep(64);
+__device__ __forceinline__ uint32_t wait_flag(const uint32_t* p, uint32_t target) {
+  uint32_t v;
+  while ((v = ld_acquire(p)) < target) __nanosleep(64);
+  return v;
 }
 
-// Debug-only progress trace (rs_debug_set_trace): one 64-bit word per (CTA, warp),
-// (round << 48) | (block << 24) | (state << 16) | position, written to mapped host memory
-// so a stalled launch can be inspected from the host while it runs. Null in production.
-// Compiled in only with -DRS_TRACE (RS_NVCC_EXTRA=-DRS_TRACE python -m paper_2412_01852_b200.build).
+// Debug-only instrumentation (compiled in with -DRS_TRACE; see rs_debug_set_trace).
+// Each unit a warp runs writes one record of kTraceWords uint64 to
+// g_trace[((cta * kMaxWarps + warp) * kTraceRounds + round) * kTraceWords]:
+//   0 unit | src<<32 | dst<<40 | smid<<48, 1 globaltimer at unit start, 2 at unit end,
+//   3 cycles waiting for self-fill / progress flags, 4 coefficient waits, 5 ring-full waits,
+//   6 ring-space waits, 7 compute (run_block), 8 post-block hand-off work, 9 blocks.
+constexpr int kTraceWords = 10;
+constexpr int kTraceRounds = 32;
 __device__ unsigned long long* g_trace = nullptr;
-__device__ __forceinline__ void trace(int warp, int jr, int b, int state, long long pos) {
-#ifndef RS_TRACE
-  (void)warp, (void)jr, (void)b, (void)state, (void)pos;
+#ifdef RS_TRACE
+__device__ __forceinline__ unsigned long long trace_clock() { return clock64(); }
+__device__ __forceinline__ unsigned long long trace_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned trace_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 #else
+__device__ __forceinline__ unsigned long long trace_clock() { return 0; }
+__device__ __forceinline__ unsigned long long trace_gtime() { return 0; }
+__device__ __forceinline__ unsigned trace_smid() { return 0; }
+#endif
+struct TraceAcc {
+  unsigned long long t0 = 0, c[6] = {0, 0, 0, 0, 0, 0};
+};
+__device__ __forceinline__ void trace_unit(int warp, int jr, long long u, int src, int dst, const TraceAcc& acc,
+                                           int blocks) {
+#ifdef RS_TRACE
   unsigned long long* t = g_trace;
-  if (t != nullptr && (threadIdx.x & 31) == 0) {
-    const unsigned long long v = ((unsigned long long)(jr & 0xffff) << 48) |
-                                 ((unsigned long long)(b & 0xffffff) << 24) |
-                                 ((unsigned long long)(state & 0xff) << 16) | (unsigned long long)(pos & 0xffff);
-    *(volatile unsigned long long*)(t + (size_t)blockIdx.x * kMaxWarps + warp) = v;
+  if (t != nullptr && (threadIdx.x & 31) == 0 && jr < kTraceRounds) {
+    unsigned long long* rec = t + (((size_t)blockIdx.x * kMaxWarps + warp) * kTraceRounds + jr) * kTraceWords;
+    rec[0] = (unsigned long long)u | ((unsigned long long)src << 32) | ((unsigned long long)dst << 40) |
+             ((unsigned long long)trace_smid() << 48);
+    rec[1] = acc.t0;
+    rec[2] = trace_gtime();
+    for (int i = 0; i < 6; ++i) rec[3 + i] = acc.c[i];
+    rec[9] = (unsigned long long)blocks;
   }
+#else
+  (void)warp, (void)jr, (void)u, (void)src, (void)dst, (void)acc, (void)blocks;
 #endif
 }
 
@@ -226,12 +261,15 @@ struct PipeParams {
   long long units;       // tiles * bands
   const void* coef;      // packed coefficient stream [bands][nblk][K+1][K]
   uint32_t* flags;       // [units] chunk-progress flags for in-place hand-offs
+  void* trash;           // 32*R elements: write/read target of lanes past the last row
   int len;               // length of the rotated dimension (n right, m left)
   int k;                 // sweeps
   int bands;             // ceil(k / K)
   int nchunk;            // ceil(len / (K+1))
   int nblk;              // nchunk + 1
   int nw;                // warps per CTA
+  int debug_no_chain;    // timing experiments only: every unit reads/writes A (wrong result)
+  int smsp_group;        // place chain neighbours on the same SM sub-partition
 };
 
 // ------------------------------------------------------------------------------------
@@ -243,10 +281,20 @@ struct PipeParams {
 template <typename T, int K, int R, bool STRICT, bool REFL, bool EDGE, bool OUTRING>
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>* __restrict__ cb,
                                           const T* __restrict__ islot, T* __restrict__ oslot,
-                                          T* const (&gline)[R], const bool (&ok)[R], long long cs,
-                                          int b, int len, int Kb, int lane, bool has_in, bool has_out) {
+                                          T* const (&grow)[R], const long long (&gcs)[R],
+                                          int b, int len, int Kb, int lane, bool has_in_rt, bool has_out_rt) {
   constexpr int TR = 32 * R;
   const long long c0 = (long long)b * (K + 1);
+  // interior blocks always have input and output; only edge blocks test at run time
+  const bool has_in = !EDGE || has_in_rt;
+  const bool has_out = !EDGE || has_out_rt;
+  // global output: one running pointer per row (rows past the matrix write a trash slot
+  // with stride 0, so the store needs no predicate)
+  T* gp[R];
+  if constexpr (!OUTRING) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) gp[r] = grow[r] + (c0 - (K + 1)) * gcs[r];
+  }
 #pragma unroll
   for (int u = 0; u <= K; ++u) {
     if (has_out) {
@@ -257,9 +305,13 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>*
           if constexpr (OUTRING) {
             oslot[u * TR + lane + 32 * r] = w[r][u];
           } else {
-            if (ok[r]) gline[r][col * cs] = w[r][u];
+            *gp[r] = w[r][u];
           }
         }
+      }
+      if constexpr (!OUTRING) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) gp[r] += gcs[r];
       }
     }
     {
@@ -308,6 +360,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
+  // Position of this warp inside a round. Chain neighbours (positions q, q+1) are placed
+  // on the same SM sub-partition (warp id mod 4) when smsp_group is set, so a consumer that
+  // waits for its producer yields the FP64 pipe to exactly that producer.
+  int qpos = warp;
+  if (P.smsp_group) {
+    const int sub = warp & 3, idx = warp >> 2;
+    int start = 0;
+    for (int s2 = 0; s2 < sub; ++s2) start += (NW - s2 + 3) / 4;
+    qpos = start + idx;
+  }
   const int lane = threadIdx.x & 31;
   CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);
   T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * CBLK);
@@ -332,15 +394,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   const int len = P.len;
   const int nchunk = P.nchunk;
   const int nblk = P.nblk;
-  uint64_t* const bar_in = bars + warp * NBAR;             // full_in[S], consumed, coef[2]
+  uint64_t* const bar_in = bars + qpos * NBAR;             // full_in[S], consumed, coef[2]
   uint64_t* const full_in = bar_in;
   uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
   uint64_t* const cbar = bar_in + S + 1;
-  uint64_t* const full_out = bars + (warp + 1) * NBAR;      // next warp's ring (only with DST_RING)
+  uint64_t* const full_out = bars + (qpos + 1) * NBAR;      // next warp's ring (only with DST_RING)
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
-  T* const rin = ring_sm + (size_t)warp * S * CHUNK;
-  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
-  CoefT* const cbuf = coef_sm + (size_t)warp * 2 * CBLK;
+  T* const rin = ring_sm + (size_t)qpos * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(qpos + 1) * S * CHUNK;
+  CoefT* const cbuf = coef_sm + (size_t)qpos * 2 * CBLK;
   constexpr uint32_t kCoefBytes = (uint32_t)(CBLK * sizeof(CoefT));
 
   // Processing order inside the CTA: when the range ends in a partial tile (its low bands
@@ -360,7 +422,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
 
   for (int jr = 0;; ++jr) {
-    const long long p = (long long)jr * NW + warp;
+    const long long p = (long long)jr * NW + qpos;
     if (p >= ue - ub) break;
     const long long u = unit_at(p);
     const long long tile = u / bands;
@@ -368,19 +430,23 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     const int Kb = min(K, P.k - band * K);
     // producer of u is u-1, consumer is u+1 (same tile); ring hand-off only when they are
     // adjacent positions of the same round of this CTA, else through A + progress flag.
-    const int src = band == 0 ? SRC_GLOBAL
-                              : ((warp > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
-    const int dst = band == bands - 1
-                        ? DST_GLOBAL
-                        : ((warp < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
+    int src = band == 0 ? SRC_GLOBAL
+                        : ((qpos > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
+    int dst = band == bands - 1 ? DST_GLOBAL
+                                : ((qpos < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
+    if (P.debug_no_chain) {
+      src = SRC_GLOBAL;
+      dst = DST_GLOBAL;
+    }
 
-    T* gline[R];
-    bool ok[R];
+    T* grow[R];        // element (row r, column 0) of this lane's lines
+    long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const long long o = tile * TR + lane + 32 * r;
-      ok[r] = o < P.owners;
-      gline[r] = A + (ok[r] ? o : 0) * P.os;
+      const bool ok = o < P.owners;
+      grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
+      gcs[r] = ok ? P.cs : 0;
     }
     const CoefT* csrc = reinterpret_cast<const CoefT*>(P.coef) + (size_t)band * nblk * CBLK;
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
@@ -392,16 +458,33 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     // self-filled input (band 0 reads A; a hand-off reads A after the producer's flag):
     // cp.async (LDGSTS) straight into this warp's own ring slot, no staging registers.
     // The slot of chunk q was last used by chunk q-S, consumed by this warp already.
+    uint32_t flag_seen = 0;  // last progress value read (poll only when it is not enough)
     auto fill_chunk = [&](int q) {
-      if (src == SRC_FLAG) wait_flag(myflag, (uint32_t)q + 1);
+      if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
       T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
+      const long long c0 = (long long)q * (K + 1);
+      const T* sp[R];
 #pragma unroll
-      for (int v = 0; v <= K; ++v) {
-        const long long col = (long long)q * (K + 1) + v;
-        const bool cv = col < len;
+      for (int r = 0; r < R; ++r) sp[r] = grow[r] + c0 * gcs[r];
+      if (c0 + K < len) {
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          cp_async_elem(dstp + v * TR + lane + 32 * r, gline[r] + (cv ? col * P.cs : 0), ok[r] && cv);
+        for (int v = 0; v <= K; ++v) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            cp_async_elem(dstp + v * TR + lane + 32 * r, sp[r], true);
+            sp[r] += gcs[r];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v <= K; ++v) {
+          const bool cv = c0 + v < len;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            cp_async_elem(dstp + v * TR + lane + 32 * r, cv ? sp[r] : grow[r], cv);
+            sp[r] += gcs[r];
+          }
+        }
       }
       cp_async_commit();
     };
@@ -410,7 +493,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_in[(seq0 + (uint32_t)q) % S]);
     };
-    trace(warp, jr, 0, 1, p);
+    TraceAcc tacc;
+    tacc.t0 = trace_gtime();
+    unsigned long long tc = trace_clock();
     if (src != SRC_RING) {
       fill_chunk(0);
       publish_chunk(0);
@@ -430,55 +515,70 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
         bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes,
                  &cbar[(cseq + 1) & 1]);
       const bool self_next = (src != SRC_RING) && (b + 1 < nchunk);
-      trace(warp, jr, b, 2, p);
+      tc = trace_clock();
       if (self_next) fill_chunk(b + 1);
-      trace(warp, jr, b, 3, p);
+      unsigned long long tn = trace_clock();
+      tacc.c[0] += tn - tc;
+      tc = tn;
 
       mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
+      tn = trace_clock();
+      tacc.c[1] += tn - tc;
+      tc = tn;
       const bool has_in = b < nchunk;
       const bool has_out = b >= 1;
       const uint32_t iseq = seq0 + (uint32_t)b;
       const T* islot = rin + (iseq % S) * CHUNK;
-      trace(warp, jr, b, 4, p);
       if (has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
-      trace(warp, jr, b, 5, p);
+      tn = trace_clock();
+      tacc.c[2] += tn - tc;
+      tc = tn;
       const uint32_t oseq = seq0 + (uint32_t)b - 1u;
       T* oslot = rout + (oseq % S) * CHUNK;
       if (dst == DST_RING && has_out && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
 
-      trace(warp, jr, b, 6, p);
+      tn = trace_clock();
+      tacc.c[3] += tn - tc;
+      tc = tn;
       const CoefT* cb = cbuf + (cseq & 1) * CBLK;
       const bool interior = b >= 1 && b <= full_hi;
       if (interior) {
         if (dst == DST_RING)
-          run_block<T, K, R, STRICT, REFL, false, true>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+          run_block<T, K, R, STRICT, REFL, false, true>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
                                                         has_in, has_out);
         else
-          run_block<T, K, R, STRICT, REFL, false, false>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+          run_block<T, K, R, STRICT, REFL, false, false>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
                                                          has_in, has_out);
       } else {
         if (dst == DST_RING)
-          run_block<T, K, R, STRICT, REFL, true, true>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+          run_block<T, K, R, STRICT, REFL, true, true>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
                                                        has_in, has_out);
         else
-          run_block<T, K, R, STRICT, REFL, true, false>(w, cb, islot, oslot, gline, ok, P.cs, b, len, Kb, lane,
+          run_block<T, K, R, STRICT, REFL, true, false>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
                                                         has_in, has_out);
       }
       __syncwarp();
+      tn = trace_clock();
+      tacc.c[4] += tn - tc;
+      tc = tn;
       if (lane == 0) {
         if (has_in) st_release_shared(consumed_in, iseq + 1u);
         if (dst == DST_RING && has_out) mbar_arrive(&full_out[oseq % S]);
       }
-      if (dst == DST_FLAG && has_out) {
+      if (dst == DST_FLAG && has_out && lane == 0 && ((b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
+        // the warp barrier above orders every lane's stores before lane 0's gpu-scope
+        // fence; the release store then publishes "chunks 0..b-1 are in A"
         __threadfence();
-        __syncwarp();
-        if (lane == 0) st_release(P.flags + u + 1, (uint32_t)b);
+        st_release(P.flags + u + 1, (uint32_t)b);
       }
       if (self_next) publish_chunk(b + 1);
       ++cseq;
+      tn = trace_clock();
+      tacc.c[5] += tn - tc;
+      tc = tn;
     }
+    trace_unit(warp, jr, u, src, dst, tacc, nblk);
   }
-  trace(warp, 0xffff, 0, 9, 0);
 }
 
 // ------------------------------------------------------------------------------------
@@ -488,24 +588,27 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
 // mirrors j and negates S (rotation) or C (reflector): both exact in IEEE arithmetic.
 // ------------------------------------------------------------------------------------
 template <typename T, int K, bool REFL>
-__global__ void rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C, const T* __restrict__ Sm,
-                               long long ldcs, int len, int k, int bands, int nblk, int rev) {
-  const long long total = (long long)bands * nblk * (K + 1) * K;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int l = (int)(e % K);
-    long long r = e / K;
-    const int u = (int)(r % (K + 1));
-    r /= (K + 1);
-    const long long b = r % nblk;
-    const int band = (int)(r / nblk);
+__global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
+                                                      const T* __restrict__ Sm, long long ldcs, int len, int k,
+                                                      int nblk, int rev) {
+  // grid.y = band; consecutive threads write consecutive records (coalesced), and each
+  // warp reads 8 coefficient columns x 4 consecutive rows (one sector per column)
+  constexpr int E = (K + 1) * K;
+  const int band = blockIdx.y;
+  const int total = nblk * E;
+  Coef<T, REFL>* dst = out + (size_t)band * total;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int b = i / E;
+    const int e = i - b * E;
+    const int u = e / K;
+    const int l = e - u * K;
     const int p = band * K + l;
-    const long long j = b * (K + 1) + u - 1 - l;
+    const int j = b * (K + 1) + u - 1 - l;
     Coef<T, REFL> cf;
-    if (p < k && j >= 0 && j <= (long long)len - 2) {
-      const long long jj = rev ? (long long)len - 2 - j : j;
-      T c = C[jj + (long long)p * ldcs];
-      T s = Sm[jj + (long long)p * ldcs];
+    if (p < k && j >= 0 && j <= len - 2) {
+      const long long jj = rev ? (long long)(len - 2 - j) : (long long)j;
+      T c = __ldg(C + jj + (long long)p * ldcs);
+      T s = __ldg(Sm + jj + (long long)p * ldcs);
       if constexpr (REFL) {
         if (rev) c = -c;
         cf.s = s;
@@ -528,7 +631,7 @@ __global__ void rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restr
         cf.s = T(0);
       }
     }
-    out[e] = cf;
+    dst[i] = cf;
   }
 }
 
@@ -597,7 +700,7 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
   g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 : 2) * tsz;
   g->coef_bytes = align_up((size_t)g->bands * g->nblk * (kK + 1) * kK * g->coef_rec, 256);
-  g->flag_bytes = align_up((size_t)(g->units + 1) * sizeof(uint32_t), 256);
+  g->flag_bytes = align_up((size_t)(g->units + 1) * sizeof(uint32_t), 256) + kTrashBytes;
   return true;
 }
 
@@ -659,14 +762,14 @@ rs_status launch_pipeline(const Geometry& g, T* Abase, const T* C, const T* S, l
   if (rc != RS_OK) return rc;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
   uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes);
-  cudaError_t e = cudaMemsetAsync(flags, 0, g.flag_bytes, st);
+  cudaError_t e = cudaMemsetAsync(flags, 0, g.flag_bytes - kTrashBytes, st);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   {
-    const long long total = (long long)g.bands * g.nblk * (kK + 1) * kK;
-    long long blocks = (total + 255) / 256;
-    if (blocks > 148LL * 16) blocks = 148LL * 16;
-    if (blocks < 1) blocks = 1;
-    rs_pack_kernel<T, kK, REFL><<<(unsigned)blocks, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.bands, g.nblk, rev);
+    const int per_band = g.nblk * (kK + 1) * kK;
+    int bx = (per_band + 255) / 256;
+    if (bx > 64) bx = 64;
+    dim3 pgrid((unsigned)bx, (unsigned)g.bands);
+    rs_pack_kernel<T, kK, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk, rev);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
@@ -680,15 +783,30 @@ rs_status launch_pipeline(const Geometry& g, T* Abase, const T* C, const T* S, l
   P.units = g.units;
   P.coef = coef;
   P.flags = flags;
+  P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flag_bytes - kTrashBytes;
   P.len = g.len;
   P.k = g.k;
   P.bands = g.bands;
   P.nchunk = g.nchunk;
   P.nblk = g.nblk;
   P.nw = lp.nw;
+  P.debug_no_chain = getenv("RS_DEBUG_NO_CHAIN") ? atoi(getenv("RS_DEBUG_NO_CHAIN")) : 0;
+  P.smsp_group = getenv("RS_SMSP_GROUP") ? atoi(getenv("RS_SMSP_GROUP")) : 1;
   auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL>;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lp.smem);
-  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  {
+    // opt in to the large dynamic shared memory once per (kernel, device)
+    static std::atomic<int> configured_mask{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int bit = 1 << (dev & 31);
+    if (!(configured_mask.load(std::memory_order_relaxed) & bit)) {
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+      if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      configured_mask.fetch_or(bit, std::memory_order_relaxed);
+    }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)lp.grid);
   cfg.blockDim = dim3((unsigned)(lp.nw * 32));
@@ -734,9 +852,9 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   if (len < 2)
     return fail(RS_EINVAL, left ? "matrix needs at least 2 rows for left-side application"
                                 : "matrix needs at least 2 columns");
-  if (len > (int64_t)1 << 30) return fail(RS_EUNSUPPORTED, "rotated dimension too long");
+  if (len > (int64_t)1 << 26) return fail(RS_EUNSUPPORTED, "rotated dimension longer than 2^26");
   if (k < 1) return fail(RS_EINVAL, "need k >= 1 sequences");
-  if (k > (int64_t)1 << 24) return fail(RS_EUNSUPPORTED, "too many sequences");
+  if (k > (int64_t)65535 * kK) return fail(RS_EUNSUPPORTED, "more than 65535*8 sequences");
   if (lda < (m > 1 ? m : 1)) return fail(RS_EINVAL, "lda must be >= max(1, m) (column-major)");
   if (ldcs < len - 1) return fail(RS_EINVAL, "ldcs must be >= len - 1");
   if (owners == 0) return RS_OK;  // no rows: no-op (blocking.py:446-447)
@@ -861,6 +979,7 @@ rs_status rs_debug_set_trace(void* device_ptr) {
   return fail(RS_EUNSUPPORTED, "library built without -DRS_TRACE");
 #endif
   unsigned long long* p = reinterpret_cast<unsigned long long*>(device_ptr);
+  (void)kTraceWords;
   cudaError_t e = cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("rs_debug_set_trace: ") + cudaGetErrorString(e));
   return RS_OK;

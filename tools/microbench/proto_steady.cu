@@ -77,10 +77,10 @@ void run(int warps_per_cta, int ctas_per_sm) {
   cudaFree(o);
 }
 int main() {
-  run<8, 1, false>(8, 1); run<8, 1, false>(16, 1); run<8, 1, false>(24, 1); run<8, 1, false>(32, 1);
-  run<8, 2, false>(8, 1); run<8, 2, false>(12, 1); run<8, 2, false>(16, 1); run<8, 2, false>(24, 1);
-  run<4, 2, false>(16, 1); run<6, 2, false>(16, 1); run<12, 1, false>(16, 1); run<16, 1, false>(16, 1);
-  run<8, 4, false>(8, 1); run<8, 4, false>(12, 1);
-  run<8, 1, true>(16, 1); run<8, 2, true>(16, 1); run<8, 2, true>(24, 1);
+  // 1 warp per SMSP (4 warps/SM) = single-warp efficiency; 2 and 3 per SMSP for reference
+  run<8, 1, false>(4, 1); run<8, 2, false>(4, 1); run<8, 4, false>(4, 1);
+  run<8, 2, false>(8, 1); run<8, 2, false>(12, 1);
+  run<12, 2, false>(4, 1); run<6, 2, false>(4, 1); run<4, 4, false>(4, 1);
+  run<8, 2, true>(4, 1); run<8, 2, true>(8, 1);
   return 0;
 }

@@ -1,0 +1,58 @@
+"""Timeline analysis of one pipeline launch (needs tools/exp/lib_trace.so, built with -DRS_TRACE)."""
+import sys, os
+HERE = os.path.dirname(os.path.abspath(__file__))
+os.environ.setdefault("RS_LIB_PATH", os.path.join(HERE, "exp", "lib_trace.so"))
+sys.path.insert(0, os.path.dirname(HERE))
+import numpy as np, torch
+from paper_2412_01852_b200 import apply_device, _lib, flops_applied
+m, n, k = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (4096, 4096, 192)
+lib = _lib.load()
+info = _lib.plan_info(m, n, k)
+G, NW = info["grid_ctas"], info["warps_per_cta"]
+W, RND = 10, 32
+buf = torch.zeros(G * 16 * RND * W, dtype=torch.int64, device="cuda")
+_lib.check(lib.rs_debug_set_trace(buf.data_ptr()), "trace")
+A = torch.randn(n, m, dtype=torch.float64, device="cuda").t()
+th = torch.rand(k, n - 1, dtype=torch.float64, device="cuda").t() * 6.283185307179586
+C, S = torch.cos(th), torch.sin(th)
+for _ in range(2):
+    buf.zero_(); apply_device(A, (C, S), fast=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+buf.zero_(); e0.record(); apply_device(A, (C, S), fast=True); e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1)
+rec = buf.cpu().numpy().reshape(G, 16, RND, W)
+valid = rec[..., 1] != 0
+r = rec[valid]
+t0 = r[:, 1].min()
+start = (r[:, 1] - t0) / 1e3
+end = (r[:, 2] - t0) / 1e3
+print(f"{m}x{n} k={k}: {ms:.3f} ms, {flops_applied(m,n,k)/ms/1e9:.2f} TF/s; grid {G} x {NW} warps; units {len(r)}")
+print(f"unit duration us: min {np.min(end-start):.1f} med {np.median(end-start):.1f} max {np.max(end-start):.1f}")
+print(f"unit start us: min {start.min():.1f} med {np.median(start):.1f} max {start.max():.1f}; end max {end.max():.1f}")
+names = ["fill/flag", "coef", "full", "space", "compute", "post"]
+tot = r[:, 3:9].sum(axis=0).astype(float)
+print("cycle shares:", ", ".join(f"{nm} {100*v/tot.sum():.1f}%" for nm, v in zip(names, tot)))
+srcs = (r[:, 0] >> 32) & 0xff
+for sv, nm in ((0, "ring"), (1, "global"), (2, "flag")):
+    sel = srcs == sv
+    if sel.any():
+        t = r[sel, 3:9].sum(axis=0).astype(float)
+        print(f"  src={nm:6s} n={sel.sum():5d}:", ", ".join(f"{a} {100*v/t.sum():.1f}%" for a, v in zip(names, t)))
+per_block_compute = r[:, 7].sum() / r[:, 9].sum()
+print(f"compute cycles per warp-block: {per_block_compute:.0f}")
+# active units over time (all SMs)
+T = end.max(); bins = np.linspace(0, T, 21)
+act = [((start < b1) & (end > b0)).sum() for b0, b1 in zip(bins[:-1], bins[1:])]
+print("active units per 5% of time:", act)
+# per-warp breakdown for a few CTAs
+print("per-warp (cta,wid,pos,unit,band,src,dst): compute% full% space% flag%  total_cycles")
+for c in (0, 1, 2, 70, 147):
+    for w in range(NW):
+        x = rec[c, w, 0]
+        if x[1] == 0: continue
+        u = int(x[0]) & 0xffffffff; srcv = (int(x[0]) >> 32) & 0xff; dstv = (int(x[0]) >> 40) & 0xff
+        cyc = x[3:9].astype(float); tt = cyc.sum()
+        print(f"  c{c:3d} w{w:2d} unit {u:5d} band {u % (k // 8):2d} src {['ring','glob','flag'][srcv]} dst {['ring','glob','flag'][dstv]}: "
+              f"comp {100*cyc[4]/tt:5.1f} full {100*cyc[2]/tt:5.1f} space {100*cyc[3]/tt:5.1f} flag {100*cyc[0]/tt:5.1f} "
+              f"start {(x[1]-t0)/1e3:7.1f} end {(x[2]-t0)/1e3:7.1f} us")
