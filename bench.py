@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 rotation-sequence apply (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 1..5] [--arith fast|strict]
+
+Workload (BASELINE.json): N=1 -> config 2 (m=n=4096, k=192, fp64, right/forward, the
+configuration the metric is quoted on); N>1 -> config 3 (65536x2048, k=256, fp64,
+row-sharded) unless --config is given. A "step" is one full application of the sequence
+(coefficient repack + band-pipeline kernel) to the whole matrix.
+
+* value     GFLOP/s (6*m*(n-1)*k per step, all ranks) with A, C, S resident in HBM;
+            per-step CUDA events on the launching stream, L2 flushed between steps
+            (a 256 MiB write), barrier + synchronize around the K timed steps, max
+            over ranks.
+* e2e       the same metric through the public host API (apply_cuda on pinned host
+            tensors): H2D of A, C, S and D2H of A inside every timed step.
+* roofline  the pipeline kernel alone (events around rs_apply_packed on the same
+            stream) against the live-measured DFMA/FFMA peak of this GPU: the path is
+            FP64/FP32-pipe bound (arithmetic intensity x HBM bandwidth >> FP peak).
+* cpu_baseline / --impl reference   the CPU oracle port of the reference's fastest tier
+            (oracle/rotseq_oracle.c, apply_blocked "kernel" tier, fast build) on all
+            host threads; the reference itself (Python + numba) is not on the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rotation-apply GFLOP/s (6*m*(n-1)*k flops) and fraction of FP64/FP32 peak"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("b200", "ours", "reference"), default="b200")
+    ap.add_argument("--config", type=int, default=None)
+    ap.add_argument("--arith", choices=("fast", "strict"), default="fast")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0, help="CPU baseline time budget")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------------
+# clocks sampling (nvidia-smi) during the timed region
+# ----------------------------------------------------------------------------------
+REASON_FIELDS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.samples = []
+        self.proc = None
+        self.gpu_index = gpu_index
+        self.active = False
+        self._thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm," + ",".join(f"clocks_event_reasons.{f}" for f in REASON_FIELDS))
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-i", str(self.gpu_index),
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self._thread = threading.Thread(target=self._reader, daemon=True)
+        self._thread.start()
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 2 + len(REASON_FIELDS):
+                continue
+            try:
+                sm, smax = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            reasons = [f for f, v in zip(REASON_FIELDS, parts[2:]) if v.lower() in ("active", "1")]
+            if self.active:
+                self.samples.append((sm, smax, reasons))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        reasons = sorted({r for s in self.samples for r in s[2]})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference's kernel tier)
+# ----------------------------------------------------------------------------------
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_reference_inputs(w, A, C, S):
+    """Map the workload onto the reference's only semantics (right side, forward,
+    fp64): left side -> transposed copy, reverse -> mirrored copy with S negated, fp32 ->
+    fp64 stand-in. The copies are made outside the timed region."""
+    from paper_2412_01852_b200 import Order, Side
+
+    A = np.asarray(A, dtype=np.float64)
+    C = np.asarray(C, dtype=np.float64)
+    S = np.asarray(S, dtype=np.float64)
+    if w.side is Side.LEFT:
+        A = A.T
+    if w.order is Order.REVERSE:
+        A = A[:, ::-1]
+        C, S = C[::-1, :], -S[::-1, :]
+    return np.asfortranarray(A), np.asfortranarray(C), np.asfortranarray(S)
+
+
+def time_cpu_reference(w, A, C, S, seconds: float, reps_min: int = 1, reps_max: int = 50):
+    """Best-of-reps oracle "kernel" tier (fast build, all host threads) on a bounded
+    row sample of the workload (the full matrix when it fits the time budget)."""
+    from oracle import oracle
+
+    threads = cpu_threads()
+    A0, C0, S0 = cpu_reference_inputs(w, A, C, S)
+    rows = A0.shape[0]
+    # size the sample: measure a 256-row probe first
+    probe_rows = min(rows, 256)
+    Ap = np.asfortranarray(A0[:probe_rows])
+    t0 = time.perf_counter()
+    oracle.apply_blocked(Ap, C0, S0, fast=True, threads=threads)
+    dt = time.perf_counter() - t0
+    est_full = dt * rows / probe_rows
+    sample_rows = rows if est_full <= seconds / 2 else max(256, int(rows * (seconds / 2) / est_full) // 128 * 128)
+    As = np.asfortranarray(A0[:sample_rows])
+    flops = 6.0 * sample_rows * (As.shape[1] - 1) * C0.shape[1]
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < reps_max:
+        work = As.copy(order="F")
+        t0 = time.perf_counter()
+        oracle.apply_blocked(work, C0, S0, fast=True, threads=threads)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= reps_min and time.perf_counter() - t_start > seconds:
+            break
+    best = min(times)
+    return {"value": flops / best / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": (f"{sample_rows} of {rows} rows x {As.shape[1]} cols, k={C0.shape[1]}, "
+                       f"best of {len(times)} reps; oracle/rotseq_oracle.c apply_blocked (reference kernel "
+                       f"tier, plan n_b/k_b/m_b from the default CacheSpec, shape 128x4, fast build)"
+                       + ("; fp64 stand-in for fp32" if w.dtype == np.float32 else "")
+                       + ("; left/reverse mapped to right/forward copies" if w.side.value == "left"
+                          or w.order.value == "reverse" else "")),
+            "seconds_per_rep": best, "sample_flops": flops}
+
+
+# ----------------------------------------------------------------------------------
+# main
+# ----------------------------------------------------------------------------------
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    n_gpus = max(args.gpus, world)
+    cfg_index = args.config if args.config is not None else (2 if n_gpus == 1 else 3)
+
+    from paper_2412_01852_b200 import WORKLOADS, Side, make_workload_inputs, shard_range
+
+    w = WORKLOADS[cfg_index]
+    fast = args.arith == "fast"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        A, C, S = make_workload_inputs(w)
+        flops = w.flops
+        threads = cpu_threads()
+        A0, C0, S0 = cpu_reference_inputs(w, A, C, S)
+        from oracle import oracle
+
+        if args.warmup > 0:  # no JIT to warm; one untimed pass touches the pages
+            oracle.apply_blocked(A0.copy(order="F"), C0, S0, fast=fast, threads=threads)
+        times = []
+        for _ in range(args.steps):
+            work = A0.copy(order="F")
+            t0 = time.perf_counter()
+            oracle.apply_blocked(work, C0, S0, fast=fast, threads=threads)
+            times.append(time.perf_counter() - t0)
+        total = sum(times)
+        value = flops * args.steps / total / 1e9
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": n_gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE seeded generators, workloads.py)",
+            "config": {"workload": w.name(), "m": w.m, "n": w.n, "k": w.k, "arith": args.arith},
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                             "sample": ("full workload matrix per step; oracle/rotseq_oracle.c apply_blocked "
+                                        "(C port of the reference kernel tier; the reference itself is "
+                                        "Python+numba and not present on the GPU box)"
+                                        + ("; fp64 stand-in for fp32" if w.dtype == np.float32 else ""))},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_01852_b200 import PackedSequence, _lib, apply_cuda
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    tdtype = torch.float64 if w.dtype == np.float64 else torch.float32
+    o0, o1 = shard_range(w.owners, world, rank, align=64)
+    # inputs: config 1/2/4/5 (and config 3 at N=1) use the exact seeded generator; for
+    # sharded config 3 every rank generates only its own rows with a rank-specific
+    # stream (same distribution; generating 1 GiB per rank would dominate start-up).
+    if world > 1 and w.index == 3:
+        g = torch.Generator(device=dev)
+        g.manual_seed(1000 + rank)
+        mloc = o1 - o0
+        dA = torch.randn(w.n, mloc, dtype=tdtype, device=dev, generator=g).t()
+        Ah = None
+        if rank == 0:
+            th = np.random.Generator(np.random.Philox(1)).uniform(0.0, 2.0 * np.pi, size=(w.n - 1, w.k))
+            Cn, Sn = np.cos(th), np.sin(th)
+        else:
+            Cn = Sn = None
+    else:
+        Ah, Cn, Sn = make_workload_inputs(w, owner_range=(o0, o1) if world > 1 else None)
+        dA = torch.empty_strided(Ah.shape, (1, max(Ah.shape[0], 1)), dtype=tdtype, device=dev)
+        dA.copy_(torch.from_numpy(Ah))
+    length = w.length
+    dC = torch.empty_strided((length - 1, w.k), (1, length - 1), dtype=tdtype, device=dev)
+    dS = torch.empty_strided((length - 1, w.k), (1, length - 1), dtype=tdtype, device=dev)
+    if rank == 0:
+        dC.copy_(torch.from_numpy(np.asfortranarray(Cn)).to(tdtype))
+        dS.copy_(torch.from_numpy(np.asfortranarray(Sn)).to(tdtype))
+    m_loc, n_loc = dA.shape
+    flops_local = (6.0 * n_loc * (m_loc - 1) * w.k) if w.side is Side.LEFT else (6.0 * m_loc * (n_loc - 1) * w.k)
+
+    def broadcast_cs():
+        if world > 1:
+            dist.broadcast(dC, src=0)
+            dist.broadcast(dS, src=0)
+
+    broadcast_cs()
+    packed = PackedSequence((dC, dS), (m_loc, n_loc), side=w.side, order=w.order, dtype=tdtype, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        broadcast_cs()
+        if evs is not None:
+            evs[0].record(stream)
+        packed.pack((dC, dS))
+        if evs is not None:
+            evs[1].record(stream)
+        packed.apply(dA, fast=fast)
+        if evs is not None:
+            evs[2].record(stream)
+
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    sampler.active = True  # clocks are sampled under load: warm-up + timed region
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize(dev)
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = _lib.launch_count()
+    sampler.active = True
+    for i in range(args.steps):
+        step(evs[i])
+        flush.zero_()
+    torch.cuda.synchronize(dev)
+    sampler.active = False
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
+    kern_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    pack_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms_max = float(t.item())
+    flops_total = w.flops if world == 1 else w.flops  # all ranks together cover the whole matrix
+    value = flops_total * args.steps / (total_ms_max * 1e-3) / 1e9
+
+    # end-to-end through the public host API (pinned host buffers, copies inside)
+    e2e = None
+    if not args.no_e2e and Ah is None:
+        Ah = dA.cpu().numpy()  # this rank's shard (column-major), as the host-side input
+    if not args.no_e2e:
+        hA = torch.empty_strided(Ah.shape, (1, max(Ah.shape[0], 1)), dtype=tdtype, pin_memory=True)
+        hA.copy_(torch.from_numpy(Ah))
+        hC = torch.empty_strided(dC.shape, (1, length - 1), dtype=tdtype, pin_memory=True)
+        hS = torch.empty_strided(dS.shape, (1, length - 1), dtype=tdtype, pin_memory=True)
+        hC.copy_(dC.cpu())
+        hS.copy_(dS.cpu())
+        for _ in range(2):
+            apply_cuda(hA, (hC, hS), fast=fast, side=w.side, order=w.order)
+        e2e_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            apply_cuda(hA, (hC, hS), fast=fast, side=w.side, order=w.order)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            e2e_ms.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        bi = hA.numel() * hA.element_size() + hC.numel() * hC.element_size() * 2
+        bo = hA.numel() * hA.element_size()
+        e2e = {"value": flops_total / (float(t.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+               "ms_per_step": float(t.item()), "api": "apply_cuda(pinned host torch tensors)"}
+
+    # roofline: the pipeline kernel against the live FMA-pipe peak
+    peak = _lib.fma_peak_tflops(_lib.DTYPE_F64 if tdtype == torch.float64 else _lib.DTYPE_F32)
+    kern_avg_ms = statistics.mean(kern_ms)
+    achieved = flops_local / (kern_avg_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"config{w.index}")
+        except (OSError, ValueError):
+            traffic = None
+    try:
+        hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+        hbm_src = "MEASURED_PEAKS.json"
+    except (OSError, ValueError, KeyError):
+        hbm, hbm_src = 6650.0, "fallback"
+    ai = w.flops / w.algorithmic_bytes()
+    roofline = {
+        "bound": "fp64" if tdtype == torch.float64 else "fp32",
+        "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+        "traffic": traffic,
+        "peak_source": f"measured live on this GPU ({'DFMA' if tdtype == torch.float64 else 'FFMA'} pipe microbenchmark, "
+                       "2 flops/FMA); MEASURED_PEAKS.json has no FP64/FP32 entry",
+        "kernel": "rs_pipeline_kernel", "kernel_ms": kern_avg_ms, "pack_ms": statistics.mean(pack_ms),
+        "algorithmic_flops_per_launch": flops_local,
+        "algorithmic_bytes_per_launch": w.algorithmic_bytes() / world,
+        "arithmetic_intensity": ai, "hbm_bound_tflops": ai * hbm / 1e3, "hbm_gbs": hbm, "hbm_source": hbm_src,
+        "instruction_ceiling_frac": 0.75 if fast else 0.5,
+    }
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and Cn is not None:
+        try:
+            cpu_baseline = time_cpu_reference(w, Ah, Cn, Sn, args.cpu_seconds)
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal
+            cpu_baseline = {"value": None, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
+                            "sample": f"failed: {exc}"}
+
+    sampler.stop()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": n_gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if tdtype == torch.float64 else "f32",
+            "data": ("synthetic: seeded Philox generators of BASELINE.json (workloads.py)"
+                     + ("; per-rank streams for the sharded config-3 matrix" if world > 1 and w.index == 3 else "")),
+            "config": {"workload": w.name(), "m": w.m, "n": w.n, "k": w.k, "side": w.side.value,
+                       "order": w.order.value, "arith": args.arith,
+                       "parallelism": f"{'row' if w.side is Side.RIGHT else 'column'}-sharded x{world}"
+                       + (", C/S NCCL broadcast per step" if world > 1 else ""),
+                       "l2": "L2 flushed between steps (256 MiB write); A alone exceeds the 126 MB L2"
+                             if w.m * w.n * w.itemsize > 126e6 else "L2 flushed between steps (256 MiB write)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": sampler.summary(),
+            "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -101,11 +101,31 @@ rs_status rs_apply_algo_f32(int algo, float* A, int64_t m, int64_t n, int64_t ld
                             int side, int order, int kind, int strict,
                             void* workspace, size_t workspace_bytes, void* stream);
 
+/* Prepacked / resident mode (the reference's apply_blocked_packed, blocking.py:479-515,
+ * and the paper's rs_kernel_v2): rs_pack_* repacks C/S into the caller's workspace
+ * (rs_workspace_bytes() bytes, 256-byte aligned) as the band-major, wave-major coefficient
+ * stream the kernel consumes; rs_apply_packed_* then applies it to A any number of times
+ * without touching C/S again. (m, n, k, side, order, kind) must match between the two.
+ * rs_apply_* is exactly rs_pack_* followed by rs_apply_packed_*. */
+rs_status rs_pack_f64(const double* C, const double* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                      int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
+rs_status rs_pack_f32(const float* C, const float* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                      int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
+rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,
+                              int kind, int strict, void* workspace, size_t workspace_bytes, void* stream);
+rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,
+                              int kind, int strict, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Launch geometry the pipeline would use for this problem on the current device
  * (for benchmarks / roofline accounting). Any out-pointer may be NULL. */
 rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype,
                        int* grid_ctas, int* warps_per_cta, int64_t* units, int* band_width,
                        int* rows_per_tile, size_t* smem_bytes);
+
+/* Measured FMA-pipe peak of the current device (TFLOP/s, 2 flops per FMA) for dtype
+ * RS_DTYPE_F64 (DFMA) or RS_DTYPE_F32 (FFMA): the roofline denominator for this
+ * FP-bound path. Synchronous (~10 ms). Not on the apply path. */
+rs_status rs_fma_peak_tflops(int dtype, double* tflops, void* stream);
 
 /* Number of pipeline / pack / naive kernel launches issued by this library since
  * process start (all threads). Used by bench.py to report gpu_launches. */

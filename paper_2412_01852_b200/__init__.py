@@ -27,7 +27,15 @@ from .compare import (  # noqa: F401
     fast_mode_tol,
     norm_preservation_tol,
 )
-from .apply import apply_blocked, apply_cuda, apply_device, apply_naive, workspace_bytes  # noqa: F401
+from .apply import (  # noqa: F401
+    PackedSequence,
+    apply_blocked,
+    apply_cuda,
+    apply_device,
+    apply_naive,
+    workspace_bytes,
+)
+from .workloads import WORKLOADS, Workload, make_workload_inputs, shard_range  # noqa: F401
 from .verification import ALGORITHMS, FAULT_ENV, run_variant  # noqa: F401
 
 __version__ = "0.1.0"

@@ -39,8 +39,13 @@ EXPORTS = (
     "rs_apply_algo_f64",
     "rs_apply_algo_f32",
     "rs_plan_info",
+    "rs_pack_f64",
+    "rs_pack_f32",
+    "rs_apply_packed_f64",
+    "rs_apply_packed_f32",
     "rs_launch_count",
     "rs_debug_set_trace",
+    "rs_fma_peak_tflops",
 )
 
 _lock = threading.Lock()
@@ -68,12 +73,22 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [i32] + apply_args
+    for name in ("rs_pack_f64", "rs_pack_f32"):
+        fn = getattr(lib, name)
+        fn.restype = i32
+        fn.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, vp, sz, vp]
+    for name in ("rs_apply_packed_f64", "rs_apply_packed_f32"):
+        fn = getattr(lib, name)
+        fn.restype = i32
+        fn.argtypes = [vp, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
     lib.rs_plan_info.restype = i32
     lib.rs_plan_info.argtypes = [i64, i64, i64, i32, i32, i32,
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i64),
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(sz)]
     lib.rs_launch_count.restype = i64
     lib.rs_launch_count.argtypes = []
+    lib.rs_fma_peak_tflops.restype = i32
+    lib.rs_fma_peak_tflops.argtypes = [i32, ctypes.POINTER(ctypes.c_double), vp]
     lib.rs_debug_set_trace.restype = i32
     lib.rs_debug_set_trace.argtypes = [vp]
     return lib
@@ -124,3 +139,10 @@ def plan_info(m: int, n: int, k: int, side: int = SIDE_RIGHT, kind: int = KIND_R
     check(st, "rs_plan_info")
     return dict(grid_ctas=grid.value, warps_per_cta=nw.value, units=units.value,
                 band_width=bw.value, rows_per_tile=rpt.value, smem_bytes=smem.value)
+
+
+def fma_peak_tflops(dtype: int = DTYPE_F64, stream=None) -> float:
+    """Live DFMA/FFMA peak of the current device (roofline denominator)."""
+    out = ctypes.c_double()
+    check(load().rs_fma_peak_tflops(dtype, ctypes.byref(out), stream), "rs_fma_peak_tflops")
+    return out.value

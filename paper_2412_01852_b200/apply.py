@@ -72,10 +72,10 @@ def _seq_arrays(seq, dtype, device):
     out = []
     for X, name in ((C, "C"), (S, "S")):
         if _is_tensor(X):
-            if X.device != device or X.dtype != dtype or X.dim() != 2 or (X.shape[0] > 1 and X.stride(0) != 1):
-                X = X.to(device=device, dtype=dtype)
-                if X.shape[0] > 1 and X.stride(0) != 1:
-                    X = X.t().contiguous().t()
+            if X.dim() != 2:
+                raise ValueError(f"{name} must be 2-D")
+            if X.device != device or X.dtype != dtype:
+                X = X.to(device=device, dtype=dtype, non_blocking=True)
             out.append(X)
         else:
             X = np.asarray(X)
@@ -186,10 +186,24 @@ def apply_cuda(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Sid
     core.py:110-117), copied to ``device`` (default cuda:current), transformed,
     copied back, synchronised. Device tensor input: see ``apply_device``.
     """
-    if _is_tensor(A):
+    torch = _torch()
+    if _is_tensor(A) and A.is_cuda:
         apply_device(A, seq, kind, fast, side, order, algo, workspace)
         return
-    torch = _torch()
+    if _is_tensor(A):
+        # host torch tensor (ideally pinned): async H2D, apply, async D2H, synchronise
+        if A.dim() != 2 or A.dtype not in (torch.float64, torch.float32):
+            raise ValueError("A must be a 2-D float64/float32 tensor")
+        if A.shape[0] > 1 and A.stride(0) != 1:
+            raise ValueError("A must be column-major (first stride 1)")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        m, n = A.shape
+        dA = torch.empty_strided((m, n), (1, max(m, 1)), dtype=A.dtype, device=dev)
+        dA.copy_(A, non_blocking=True)
+        apply_device(dA, seq, kind, fast, side, order, algo, workspace)
+        A.copy_(dA, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return
     kind = _as_enum(kind, TransformKind, "kind")
     side = _as_enum(side, Side, "side")
     order = _as_enum(order, Order, "order")
@@ -226,3 +240,82 @@ def apply_blocked(A, seq: RotationSequence, plan=None, shape=None, kind=Transfor
     if threads < 1:
         raise ValueError(f"threads must be >= 1, got {threads}")
     apply_cuda(A, seq, kind=kind, fast=fast)
+
+
+class PackedSequence:
+    """Coefficients packed once into device memory for repeated application.
+
+    GPU counterpart of the reference's prepacked path (``apply_blocked_packed``,
+    blocking.py:479-515; the paper's rs_kernel_v2): ``pack`` runs the
+    repack kernel into a persistent workspace, ``apply`` runs only the pipeline kernel
+    on a device-resident A. Shape, side, order and kind are fixed at construction.
+    """
+
+    def __init__(self, seq, shape, kind=TransformKind.ROTATION, side=Side.RIGHT, order=Order.FORWARD,
+                 dtype=None, device=None, stream=None):
+        torch = _torch()
+        self.kind = _as_enum(kind, TransformKind, "kind")
+        self.side = _as_enum(side, Side, "side")
+        self.order = _as_enum(order, Order, "order")
+        self.m, self.n = int(shape[0]), int(shape[1])
+        self.length = self.m if self.side is Side.LEFT else self.n
+        ncols = _seq_ncols(seq)
+        what = "rows" if self.side is Side.LEFT else "columns"
+        if self.length < 2:
+            raise ValueError(f"matrix needs at least 2 {what}")
+        if ncols != self.length:
+            raise ValueError(f"sequence acts on {ncols} {what} but matrix has {self.length}")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dtype is None:
+            dtype = torch.float64
+        self.dtype = dtype
+        self.f64 = dtype == torch.float64
+        lib = _lib.load()
+        self._side = _lib.SIDE_LEFT if self.side is Side.LEFT else _lib.SIDE_RIGHT
+        self._kind = _lib.KIND_REFLECTOR if self.kind is TransformKind.REFLECTOR else _lib.KIND_ROTATION
+        self._order = _lib.ORDER_REVERSE if self.order is Order.REVERSE else _lib.ORDER_FORWARD
+        C, S = _seq_arrays(seq, dtype, self.device)
+        self.k = int(C.shape[1])
+        nbytes = lib.rs_workspace_bytes(self.m, self.n, self.k, self._side, self._kind,
+                                        _lib.DTYPE_F64 if self.f64 else _lib.DTYPE_F32)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.pack((C, S), stream)
+
+    def _stream(self, stream):
+        torch = _torch()
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def pack(self, seq, stream=None) -> None:
+        """(Re)pack new coefficients of the same shape into the workspace."""
+        torch = _torch()
+        C, S = _seq_arrays(seq, self.dtype, self.device)
+        if tuple(C.shape) != (self.length - 1, self.k):
+            raise ValueError(f"C/S must be {(self.length - 1, self.k)}, got {tuple(C.shape)}")
+        if not all(X.shape[0] <= 1 or X.stride(0) == 1 for X in (C, S)) or C.stride(1) != S.stride(1):
+            C, S = C.t().contiguous().t(), S.t().contiguous().t()
+        ldcs = int(C.stride(1)) if self.k > 1 else max(self.length - 1, 1)
+        lib = _lib.load()
+        fn = lib.rs_pack_f64 if self.f64 else lib.rs_pack_f32
+        with torch.cuda.device(self.device):
+            st = fn(C.data_ptr(), S.data_ptr(), ldcs, self.m, self.n, self.k, self._side, self._order, self._kind,
+                    self.workspace.data_ptr(), self.workspace.numel(), self._stream(stream))
+        _lib.check(st, "rs_pack")
+
+    def apply(self, A, fast: bool = False, stream=None) -> None:
+        """Apply the packed sequence to the CUDA tensor A (column-major) in place."""
+        torch = _torch()
+        if not _is_tensor(A) or not A.is_cuda or A.dtype != self.dtype:
+            raise ValueError("A must be a CUDA tensor of the packed dtype")
+        if tuple(A.shape) != (self.m, self.n):
+            raise ValueError(f"A must have shape {(self.m, self.n)}, got {tuple(A.shape)}")
+        if self.m > 1 and A.stride(0) != 1:
+            raise ValueError("A must be column-major (first stride 1)")
+        lda = int(A.stride(1)) if self.n > 1 else max(self.m, 1)
+        lib = _lib.load()
+        fn = lib.rs_apply_packed_f64 if self.f64 else lib.rs_apply_packed_f32
+        with torch.cuda.device(self.device):
+            st = fn(A.data_ptr(), self.m, self.n, lda, self.k, self._side, self._order, self._kind,
+                    0 if fast else 1, self.workspace.data_ptr(), self.workspace.numel(), self._stream(stream))
+        _lib.check(st, "rs_apply_packed")

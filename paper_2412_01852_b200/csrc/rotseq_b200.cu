@@ -753,9 +753,26 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   return RS_OK;
 }
 
+template <typename T, bool REFL>
+rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs, int rev, void* ws,
+                      cudaStream_t st) {
+  using CoefT = Coef<T, REFL>;
+  CoefT* coef = reinterpret_cast<CoefT*>(ws);
+  const int per_band = g.nblk * (kK + 1) * kK;
+  int bx = (per_band + 255) / 256;
+  if (bx > 64) bx = 64;
+  dim3 pgrid((unsigned)bx, (unsigned)g.bands);
+  rs_pack_kernel<T, kK, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk, rev);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
+  return RS_OK;
+}
+
+// Runs the pipeline on coefficients already packed into `ws` (by launch_pack with the
+// same geometry, order and kind). Resets the hand-off flags first.
 template <typename T, bool STRICT, bool REFL>
-rs_status launch_pipeline(const Geometry& g, T* Abase, const T* C, const T* S, long long ldcs, int rev,
-                          void* ws, cudaStream_t st) {
+rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st) {
   using CoefT = Coef<T, REFL>;
   LaunchPlan lp;
   rs_status rc = plan_launch(g, sizeof(T), &lp);
@@ -764,16 +781,6 @@ rs_status launch_pipeline(const Geometry& g, T* Abase, const T* C, const T* S, l
   uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes);
   cudaError_t e = cudaMemsetAsync(flags, 0, g.flag_bytes - kTrashBytes, st);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
-  {
-    const int per_band = g.nblk * (kK + 1) * kK;
-    int bx = (per_band + 255) / 256;
-    if (bx > 64) bx = 64;
-    dim3 pgrid((unsigned)bx, (unsigned)g.bands);
-    rs_pack_kernel<T, kK, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk, rev);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
-  }
   PipeParams P;
   P.A = Abase;
   P.os = g.os;
@@ -835,20 +842,26 @@ rs_status launch_naive(const Geometry& g, T* A, const T* C, const T* S, long lon
 }
 
 template <typename T>
-rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs,
-                     int64_t k, int side, int order, int kind, int strict, void* workspace, size_t ws_bytes,
-                     void* stream) {
-  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+rs_status run_dispatch(const Geometry& g, T* A, int rev, int kind, int strict, void* ws, cudaStream_t st) {
+  if (strict)
+    return kind == RS_KIND_REFLECTOR ? launch_run<T, true, true>(g, A, rev, ws, st)
+                                     : launch_run<T, true, false>(g, A, rev, ws, st);
+  return kind == RS_KIND_REFLECTOR ? launch_run<T, false, true>(g, A, rev, ws, st)
+                                   : launch_run<T, false, false>(g, A, rev, ws, st);
+}
+
+// Shared argument validation (reference: require_colmajor core.py:41-51, _check_apply_args
+// core.py:110-117). Returns RS_OK and fills g, or an error.
+rs_status validate(int64_t m, int64_t n, int64_t lda, int64_t ldcs, int64_t k, int side, int order, int kind,
+                   int dtype, bool need_ldcs, Geometry* g) {
   if (side != RS_SIDE_RIGHT && side != RS_SIDE_LEFT) return fail(RS_EINVAL, "side must be 0 (right) or 1 (left)");
   if (order != RS_ORDER_FORWARD && order != RS_ORDER_REVERSE)
     return fail(RS_EINVAL, "order must be 0 (forward) or 1 (reverse)");
   if (kind != RS_KIND_ROTATION && kind != RS_KIND_REFLECTOR)
     return fail(RS_EINVAL, "kind must be 0 (rotation) or 1 (reflector)");
-  if (algo != RS_ALGO_PIPELINE && algo != RS_ALGO_NAIVE) return fail(RS_EINVAL, "unknown algorithm");
   if (m < 0 || n < 0) return fail(RS_EINVAL, "matrix dimensions must be non-negative");
   const bool left = side == RS_SIDE_LEFT;
   const int64_t len = left ? m : n;
-  const int64_t owners = left ? n : m;
   if (len < 2)
     return fail(RS_EINVAL, left ? "matrix needs at least 2 rows for left-side application"
                                 : "matrix needs at least 2 columns");
@@ -856,11 +869,59 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   if (k < 1) return fail(RS_EINVAL, "need k >= 1 sequences");
   if (k > (int64_t)65535 * kK) return fail(RS_EUNSUPPORTED, "more than 65535*8 sequences");
   if (lda < (m > 1 ? m : 1)) return fail(RS_EINVAL, "lda must be >= max(1, m) (column-major)");
-  if (ldcs < len - 1) return fail(RS_EINVAL, "ldcs must be >= len - 1");
-  if (owners == 0) return RS_OK;  // no rows: no-op (blocking.py:446-447)
-  if (!A || !C || !S) return fail(RS_EINVAL, "null pointer");
+  if (need_ldcs && ldcs < len - 1) return fail(RS_EINVAL, "ldcs must be >= len - 1");
+  make_geometry(m, n, lda, k, side, kind, dtype, g);
+  return RS_OK;
+}
+
+rs_status check_workspace(const Geometry& g, void* ws, size_t bytes) {
+  if (ws == nullptr) return fail(RS_EINVAL, "packed mode needs a caller workspace");
+  if (bytes < g.coef_bytes + g.flag_bytes) return fail(RS_ENOMEM, "workspace smaller than rs_workspace_bytes()");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(RS_EINVAL, "workspace must be 256-byte aligned");
+  return RS_OK;
+}
+
+template <typename T>
+rs_status pack_impl(const T* C, const T* S, int64_t ldcs, int64_t m, int64_t n, int64_t k, int side, int order,
+                    int kind, void* ws, size_t bytes, void* stream) {
   Geometry g;
-  make_geometry(m, n, lda, k, side, kind, dtype, &g);
+  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+  rs_status rc = validate(m, n, m > 1 ? m : 1, ldcs, k, side, order, kind, dtype, true, &g);
+  if (rc != RS_OK) return rc;
+  if (!C || !S) return fail(RS_EINVAL, "null pointer");
+  rc = check_workspace(g, ws, bytes);
+  if (rc != RS_OK) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int rev = order == RS_ORDER_REVERSE;
+  return kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st)
+                                   : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st);
+}
+
+template <typename T>
+rs_status apply_packed_impl(T* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order, int kind,
+                            int strict, void* ws, size_t bytes, void* stream) {
+  Geometry g;
+  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+  rs_status rc = validate(m, n, lda, 0, k, side, order, kind, dtype, false, &g);
+  if (rc != RS_OK) return rc;
+  if (g.owners == 0) return RS_OK;
+  if (!A) return fail(RS_EINVAL, "null pointer");
+  rc = check_workspace(g, ws, bytes);
+  if (rc != RS_OK) return rc;
+  return run_dispatch<T>(g, A, order == RS_ORDER_REVERSE, kind, strict, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+template <typename T>
+rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs,
+                     int64_t k, int side, int order, int kind, int strict, void* workspace, size_t ws_bytes,
+                     void* stream) {
+  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+  if (algo != RS_ALGO_PIPELINE && algo != RS_ALGO_NAIVE) return fail(RS_EINVAL, "unknown algorithm");
+  Geometry g;
+  rs_status vrc = validate(m, n, lda, ldcs, k, side, order, kind, dtype, true, &g);
+  if (vrc != RS_OK) return vrc;
+  if (g.owners == 0) return RS_OK;  // no rows: no-op (blocking.py:446-447)
+  if (!A || !C || !S) return fail(RS_EINVAL, "null pointer");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int rev = order == RS_ORDER_REVERSE;
   if (algo == RS_ALGO_NAIVE) {
@@ -883,14 +944,9 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   } else if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) {
     return fail(RS_EINVAL, "workspace must be 256-byte aligned");
   }
-  rs_status rc;
-  if (strict) {
-    rc = kind == RS_KIND_REFLECTOR ? launch_pipeline<T, true, true>(g, A, C, S, ldcs, rev, ws, st)
-                                   : launch_pipeline<T, true, false>(g, A, C, S, ldcs, rev, ws, st);
-  } else {
-    rc = kind == RS_KIND_REFLECTOR ? launch_pipeline<T, false, true>(g, A, C, S, ldcs, rev, ws, st)
-                                   : launch_pipeline<T, false, false>(g, A, C, S, ldcs, rev, ws, st);
-  }
+  rs_status rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st)
+                                           : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st);
+  if (rc == RS_OK) rc = run_dispatch<T>(g, A, rev, kind, strict, ws, st);
   if (owned) {
     cudaError_t e = cudaFreeAsync(ws, st);
     if (rc == RS_OK && e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFreeAsync: ") + cudaGetErrorString(e));
@@ -898,9 +954,66 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   return rc;
 }
 
+// ------------------------------------------------------------------------------------
+// FMA-pipe peak probe (roofline denominator: MEASURED_PEAKS.json has no FP64/FP32 entry)
+// ------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) rs_fma_peak_kernel(T* out, int iters, T a, T b) {
+  T acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = (T)(threadIdx.x + c);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = fma_rn(acc[c], a, b);
+  }
+  T s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += acc[c];
+  if (s == (T)-1.2345) out[0] = s;
+}
+
+template <typename T>
+rs_status fma_peak(double* tflops, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  T* out = nullptr;
+  if (cudaMallocAsync(&out, 64, st) != cudaSuccess) return fail(RS_ENOMEM, "peak probe allocation");
+  const int iters = sizeof(T) == 8 ? 20000 : 40000;
+  const int blocks = sms * 8, threads = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  rs_fma_peak_kernel<T><<<blocks, threads, 0, st>>>(out, iters, (T)0.999, (T)0.001);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, st);
+    rs_fma_peak_kernel<T><<<blocks, threads, 0, st>>>(out, iters, (T)0.999, (T)0.001);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(out, st);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("peak probe: ") + cudaGetErrorString(e));
+  *tflops = 2.0 * 8.0 * (double)iters * blocks * threads / (best * 1e-3) / 1e12;
+  return RS_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+rs_status rs_fma_peak_tflops(int dtype, double* tflops, void* stream) {
+  g_err.clear();
+  if (!tflops) return fail(RS_EINVAL, "null pointer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return dtype == RS_DTYPE_F32 ? fma_peak<float>(tflops, st) : fma_peak<double>(tflops, st);
+}
 
 int rs_version(void) { return RS_VERSION; }
 
@@ -971,6 +1084,27 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
 }
 
 int64_t rs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+rs_status rs_pack_f64(const double* C, const double* S, int64_t ldcs, int64_t m, int64_t n, int64_t k, int side,
+                      int order, int kind, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return pack_impl<double>(C, S, ldcs, m, n, k, side, order, kind, workspace, workspace_bytes, stream);
+}
+rs_status rs_pack_f32(const float* C, const float* S, int64_t ldcs, int64_t m, int64_t n, int64_t k, int side,
+                      int order, int kind, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return pack_impl<float>(C, S, ldcs, m, n, k, side, order, kind, workspace, workspace_bytes, stream);
+}
+rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order, int kind,
+                              int strict, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return apply_packed_impl<double>(A, m, n, lda, k, side, order, kind, strict, workspace, workspace_bytes, stream);
+}
+rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order, int kind,
+                              int strict, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return apply_packed_impl<float>(A, m, n, lda, k, side, order, kind, strict, workspace, workspace_bytes, stream);
+}
 
 rs_status rs_debug_set_trace(void* device_ptr) {
   g_err.clear();
