@@ -140,9 +140,15 @@ def partition_rows(m: int, threads: int, m_r: int):
 
 def numpy_apply_naive(A, C, S, side: str = "right", order: str = "forward", kind: str = "rotation") -> None:
     """Pure-numpy restatement of _naive_py (core.py:195-205) + extensions; strict
-    IEEE arithmetic (numpy never contracts), vectorised across owners."""
-    _check_A(A)
-    C, S = _cs(C, S)
+    IEEE arithmetic (numpy never contracts), vectorised across owners. Works in the
+    dtype of A: float64 (the reference) or float32 (the strict fp32 oracle, with C/S
+    rounded to float32)."""
+    if not isinstance(A, np.ndarray) or A.ndim != 2 or A.dtype not in (np.float64, np.float32):
+        raise ValueError("oracle works on 2-D float64/float32 arrays")
+    if A.shape[0] > 1 and A.strides[0] != A.itemsize:
+        raise ValueError("A must be column-major")
+    C = np.asfortranarray(C, dtype=A.dtype)
+    S = np.asfortranarray(S, dtype=A.dtype)
     X = A.T if side == "left" else A  # lines are columns of X, owners its rows
     length = X.shape[1]
     for p in range(C.shape[1]):

@@ -17,6 +17,9 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 
+FLAG_EVERY = 4  # kFlagEvery in rotseq_b200.cu
+
+
 @dataclass
 class Geometry:
     owners: int
@@ -49,6 +52,14 @@ class Geometry:
     @property
     def nblk(self):
         return self.nchunk + 1
+
+
+def warp_cap(dtype_bytes: int = 8, refl: bool = False, R: int = 2, K: int = 8, S: int = 3,
+             optin: int = 232448, max_warps: int = 16) -> int:
+    """plan_launch()'s shared-memory bound on warps per CTA."""
+    rec = (4 if refl else 2) * dtype_bytes
+    per = 2 * (K + 1) * K * rec + S * (K + 1) * 32 * R * dtype_bytes + (S + 3) * 8
+    return min(max_warps, (optin - (S + 3) * 8) // per)
 
 
 def plan(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None):
@@ -178,7 +189,7 @@ def simulate(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None
                 arrivals_empty[ring_in] = ea(ring_in) + 1
             if dst == "ring" and has_out:
                 arrivals_full[ring_out] = fa(ring_out) + 1
-            if dst == "flag" and has_out:
+            if dst == "flag" and has_out and (b % FLAG_EVERY == 0 or b == nblk - 1):
                 flags[u + 1] = b
             if self_next:
                 arrivals_full[ring_in] = fa(ring_in) + 1
@@ -209,3 +220,16 @@ def check_band_block_order(g: Geometry, order: dict):
                 # chunk b of band `band` input = output chunk b of band-1, emitted in its block b+1
                 prev = done.get(band - 1, -1)
                 assert prev >= min(b + 1, g.nblk - 1), (tile, band, b, prev)
+
+
+def block_rotations(g: Geometry, band: int, b: int):
+    """Rotations (j, p) of block b of a band, in the kernel's order (run_block):
+    wave u = 0..K (t = b(K+1)+u-1), lanes l ascending, j = t - l."""
+    K = g.K
+    kb = min(K, g.k - band * K)
+    for u in range(K + 1):
+        t = b * (K + 1) + u - 1
+        for lane in range(kb):
+            j = t - lane
+            if 0 <= j <= g.length - 2:
+                yield j, band * K + lane

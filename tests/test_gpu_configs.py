@@ -1,0 +1,119 @@
+"""BASELINE.json configs 1-5 at full size on the GPU.
+
+Full-size parity uses what the domain allows: rows (right side) / columns (left
+side) are independent, so a seeded subset of owners is checked bit for bit against
+the CPU oracle in strict mode, and the whole matrix is checked through
+size-independent properties (norm preservation, GPU-count/shard invariance, strict
+vs. fast within 10*k*eps). Config 2 is compared in full against the oracle's
+kernel tier on all host cores."""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def _threads():
+    return len(os.sched_getaffinity(0))
+
+
+def _device_apply(A, C, S, w, fast):
+    import torch
+
+    from paper_2412_01852_b200 import apply_device
+
+    tdt = torch.float64 if A.dtype == np.float64 else torch.float32
+    dA = torch.empty_strided(A.shape, (1, A.shape[0]), dtype=tdt, device="cuda")
+    dA.copy_(torch.from_numpy(A))
+    apply_device(dA, (torch.from_numpy(C).to(tdt), torch.from_numpy(S).to(tdt)), fast=fast, side=w.side,
+                 order=w.order)
+    return dA.cpu().numpy()
+
+
+def _owner_subset(n_owners, count, seed=0):
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(n_owners, size=min(count, n_owners), replace=False))
+    return idx
+
+
+def _oracle_subset(oracle_mod, w, A, C, S, idx):
+    """Oracle on the selected owners only (rows independent on the right side,
+    columns on the left)."""
+    sub = np.asfortranarray(A[:, idx] if w.side.value == "left" else A[idx, :]).astype(np.float64)
+    oracle_mod.apply_naive(sub, C.astype(np.float64), S.astype(np.float64), side=w.side.value,
+                           order=w.order.value)
+    return sub
+
+
+def _take(X, w, idx):
+    return np.asfortranarray(X[:, idx] if w.side.value == "left" else X[idx, :])
+
+
+def test_config1_exact(cuda, oracle_mod):
+    from paper_2412_01852_b200 import WORKLOADS, compare, make_workload_inputs
+
+    w = WORKLOADS[1]
+    A, C, S = make_workload_inputs(w)
+    ref = A.copy(order="F")
+    oracle_mod.apply_naive(ref, C, S)
+    assert_bitwise(ref, _device_apply(A, C, S, w, fast=False))
+    assert compare(ref, _device_apply(A, C, S, w, fast=True), "baseline", k=w.k).passed
+
+
+def test_config2_full_matrix(cuda, oracle_mod):
+    from paper_2412_01852_b200 import WORKLOADS, compare, make_workload_inputs
+
+    w = WORKLOADS[2]
+    A, C, S = make_workload_inputs(w)
+    ref = A.copy(order="F")
+    oracle_mod.apply_blocked(ref, C, S, threads=_threads())  # strict kernel tier == naive bitwise
+    assert_bitwise(ref, _device_apply(A, C, S, w, fast=False), "config 2 strict")
+    rep = compare(ref, _device_apply(A, C, S, w, fast=True), "baseline", k=w.k)
+    assert rep.passed, rep
+
+
+@pytest.mark.parametrize("cfg", (3, 4, 5))
+def test_full_size_subset_parity_and_invariants(cuda, oracle_mod, cfg):
+    import torch
+
+    from paper_2412_01852_b200 import WORKLOADS, baseline_tol, make_workload_inputs, shard_range
+
+    w = WORKLOADS[cfg]
+    A, C, S = make_workload_inputs(w)
+    strict = _device_apply(A, C, S, w, fast=False)
+    fast = _device_apply(A, C, S, w, fast=True)
+    idx = _owner_subset(w.owners, 96 if cfg != 5 else 48, seed=cfg)
+    # 1. strict, subset of owners, bit for bit (fp32: the numpy fp32 oracle)
+    if w.dtype == np.float64:
+        ref = _oracle_subset(oracle_mod, w, A, C, S, idx)
+        assert_bitwise(ref, _take(strict, w, idx), f"config {cfg} strict subset")
+    else:
+        sub = _take(A, w, idx)
+        oracle_mod.numpy_apply_naive(sub, C, S, side=w.side.value, order=w.order.value)
+        assert_bitwise(sub, _take(strict, w, idx), "config 4 strict fp32 subset")
+        ref = _oracle_subset(oracle_mod, w, A, C, S, idx)  # fp64 reference on fp32 inputs
+    # 2. fast, subset, within BASELINE's 10*k*eps of the working dtype
+    got = _take(fast, w, idx).astype(np.float64)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= baseline_tol(w.k, w.dtype), err
+    # 3. whole matrix: strict vs fast within tolerance; norm preservation (100*k*eps)
+    X, Y = strict.astype(np.float64), fast.astype(np.float64)
+    assert np.linalg.norm(X - Y) / np.linalg.norm(X) <= baseline_tol(w.k, w.dtype)
+    eps = float(np.finfo(w.dtype).eps)
+    nA = np.linalg.norm(A.astype(np.float64))
+    assert abs(np.linalg.norm(X) - nA) <= 100 * w.k * eps * nA
+    # 4. GPU-count invariance: 8 shards applied separately == the whole, bitwise
+    parts = []
+    for r in range(8):
+        o0, o1 = shard_range(w.owners, 8, r)
+        sh = np.asfortranarray(A[:, o0:o1] if w.side.value == "left" else A[o0:o1, :])
+        parts.append(_device_apply(sh, C, S, w, fast=False))
+    whole = np.concatenate(parts, axis=1 if w.side.value == "left" else 0)
+    assert_bitwise(strict, np.asfortranarray(whole), f"config {cfg} shard invariance")
+    torch.cuda.empty_cache()
