@@ -58,7 +58,7 @@ constexpr int kStages = RS_STAGES;  // ring depth in chunks of K+1 columns
 constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
 constexpr int kTileOwners = 32 * kR;
 constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
-constexpr int kFlagEvery = 4;   // hand-off progress is published every 4 blocks (fence cost)
+constexpr int kFlagEvery = 8;   // hand-off progress is published every 8 blocks (fence cost)
 constexpr size_t kTrashBytes = 32 * kR * 8;  // scratch slot per lane for rows past the matrix
 
 enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
@@ -177,7 +177,10 @@ __device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool valid) 
   }
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -270,6 +273,7 @@ struct PipeParams {
   int nw;                // warps per CTA
   int debug_no_chain;    // timing experiments only: every unit reads/writes A (wrong result)
   int smsp_group;        // place chain neighbours on the same SM sub-partition
+  int elastic;           // rings only within a sub-partition group, flags across
 };
 
 // ------------------------------------------------------------------------------------
@@ -365,11 +369,42 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   // waits for its producer yields the FP64 pipe to exactly that producer.
   int qpos = warp;
   if (P.smsp_group) {
+    // Balance the positions actually used in the first round (n_eff <= NW) over the four
+    // sub-partitions (e.g. 10 units -> 3,3,2,2 rather than 3,3,3,1); idle warps take the
+    // remaining positions.
+    const long long U0 = P.units * (long long)blockIdx.x / gridDim.x;
+    const long long U1 = P.units * (long long)(blockIdx.x + 1) / gridDim.x;
+    const int n_eff = (int)min((long long)NW, U1 - U0);
     const int sub = warp & 3, idx = warp >> 2;
-    int start = 0;
-    for (int s2 = 0; s2 < sub; ++s2) start += (NW - s2 + 3) / 4;
-    qpos = start + idx;
+    int act_start = 0, idle_start = 0;
+    for (int s2 = 0; s2 < sub; ++s2) {
+      const int c = (n_eff - s2 + 3) / 4;
+      act_start += c;
+      idle_start += (NW - s2 + 3) / 4 - c;
+    }
+    const int c_sub = (n_eff - sub + 3) / 4;
+    // the warp scheduler favours higher warp ids; with smsp_group == 2 the upstream
+    // (producer) end of each group gets the highest id so rings stay filled
+    const int idx2 = (P.smsp_group == 2 && idx < c_sub) ? c_sub - 1 - idx : idx;
+    qpos = idx2 < c_sub ? act_start + idx2 : n_eff + idle_start + (idx2 - c_sub);
   }
+  // Sub-partition group of a position (positions of one group share an SMSP). With
+  // P.elastic, ring hand-offs are kept only inside a group; across groups the chain goes
+  // through A + progress flags, whose unbounded slack lets every SMSP run at its own pace.
+  auto group_of = [&](int q) -> int {
+    if (!P.smsp_group) return q;
+    const long long U0 = P.units * (long long)blockIdx.x / gridDim.x;
+    const long long U1 = P.units * (long long)(blockIdx.x + 1) / gridDim.x;
+    const int n_eff = (int)min((long long)NW, U1 - U0);
+    int start = 0;
+    for (int s2 = 0; s2 < 4; ++s2) {
+      start += (n_eff - s2 + 3) / 4;
+      if (q < start) return s2;
+    }
+    return 4 + q;
+  };
+  const bool ring_from_prev = qpos > 0 && (!P.elastic || group_of(qpos - 1) == group_of(qpos));
+  const bool ring_to_next = qpos < NW - 1 && (!P.elastic || group_of(qpos) == group_of(qpos + 1));
   const int lane = threadIdx.x & 31;
   CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);
   T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * CBLK);
@@ -431,9 +466,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     // producer of u is u-1, consumer is u+1 (same tile); ring hand-off only when they are
     // adjacent positions of the same round of this CTA, else through A + progress flag.
     int src = band == 0 ? SRC_GLOBAL
-                        : ((qpos > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
+                        : ((ring_from_prev && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
     int dst = band == bands - 1 ? DST_GLOBAL
-                                : ((qpos < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
+                                : ((ring_to_next && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
     if (P.debug_no_chain) {
       src = SRC_GLOBAL;
       dst = DST_GLOBAL;
@@ -488,8 +523,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       }
       cp_async_commit();
     };
-    auto publish_chunk = [&](int q) {
-      cp_async_wait_all();
+    // chunk q is published once its cp.async group completed; one younger group (q+1)
+    // may still be in flight (two-chunk-ahead prefetch: slot of q+2 = slot of q-1)
+    auto publish_chunk = [&](int q, bool younger_in_flight) {
+      if (younger_in_flight)
+        cp_async_wait_group<1>();
+      else
+        cp_async_wait_group<0>();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_in[(seq0 + (uint32_t)q) % S]);
     };
@@ -498,7 +538,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     unsigned long long tc = trace_clock();
     if (src != SRC_RING) {
       fill_chunk(0);
-      publish_chunk(0);
+      if (1 < nchunk) fill_chunk(1);
+      publish_chunk(0, 1 < nchunk);
     }
 
     T w[R][K + 1];
@@ -515,8 +556,9 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
         bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes,
                  &cbar[(cseq + 1) & 1]);
       const bool self_next = (src != SRC_RING) && (b + 1 < nchunk);
+      const bool self_next2 = (src != SRC_RING) && (b + 2 < nchunk);
       tc = trace_clock();
-      if (self_next) fill_chunk(b + 1);
+      if (self_next2) fill_chunk(b + 2);
       unsigned long long tn = trace_clock();
       tacc.c[0] += tn - tc;
       tc = tn;
@@ -568,10 +610,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       if (dst == DST_FLAG && has_out && lane == 0 && ((b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
         // the warp barrier above orders every lane's stores before lane 0's gpu-scope
         // fence; the release store then publishes "chunks 0..b-1 are in A"
-        __threadfence();
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
         st_release(P.flags + u + 1, (uint32_t)b);
       }
-      if (self_next) publish_chunk(b + 1);
+      if (self_next) publish_chunk(b + 1, self_next2);
       ++cseq;
       tn = trace_clock();
       tacc.c[5] += tn - tc;
@@ -799,6 +841,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.nw = lp.nw;
   P.debug_no_chain = getenv("RS_DEBUG_NO_CHAIN") ? atoi(getenv("RS_DEBUG_NO_CHAIN")) : 0;
   P.smsp_group = getenv("RS_SMSP_GROUP") ? atoi(getenv("RS_SMSP_GROUP")) : 1;
+  P.elastic = getenv("RS_ELASTIC") ? atoi(getenv("RS_ELASTIC")) : 0;
   auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL>;
   {
     // opt in to the large dynamic shared memory once per (kernel, device)

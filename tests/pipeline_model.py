@@ -17,7 +17,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 
-FLAG_EVERY = 4  # kFlagEvery in rotseq_b200.cu
+FLAG_EVERY = 8  # kFlagEvery in rotseq_b200.cu
 
 
 @dataclass
@@ -165,7 +165,7 @@ def simulate(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None
             if ws.b == -1:
                 # prologue: self-fill chunk 0
                 if src != "ring":
-                    if src == "flag" and flags.get(u, 0) < 1:
+                    if src == "flag" and flags.get(u, 0) < min(2, nchunk):
                         continue
                     arrivals_full[ring_in] = fa(ring_in) + 1
                 ws.b = 0
@@ -173,7 +173,8 @@ def simulate(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None
                 continue
             b = ws.b
             self_next = src != "ring" and b + 1 < nchunk
-            if self_next and src == "flag" and flags.get(u, 0) < b + 2:
+            self_next2 = src != "ring" and b + 2 < nchunk
+            if self_next2 and src == "flag" and flags.get(u, 0) < b + 3:
                 continue
             has_in, has_out = b < nchunk, b >= 1
             iseq = seq0 + b

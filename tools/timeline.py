@@ -47,7 +47,7 @@ act = [((start < b1) & (end > b0)).sum() for b0, b1 in zip(bins[:-1], bins[1:])]
 print("active units per 5% of time:", act)
 # per-warp breakdown for a few CTAs
 print("per-warp (cta,wid,pos,unit,band,src,dst): compute% full% space% flag%  total_cycles")
-for c in (0, 1, 2, 70, 147):
+for c in [int(x) for x in os.environ.get("CTAS", "0,1,2,3").split(",")]:
     for w in range(NW):
         x = rec[c, w, 0]
         if x[1] == 0: continue
@@ -56,3 +56,13 @@ for c in (0, 1, 2, 70, 147):
         print(f"  c{c:3d} w{w:2d} unit {u:5d} band {u % (k // 8):2d} src {['ring','glob','flag'][srcv]} dst {['ring','glob','flag'][dstv]}: "
               f"comp {100*cyc[4]/tt:5.1f} full {100*cyc[2]/tt:5.1f} space {100*cyc[3]/tt:5.1f} flag {100*cyc[0]/tt:5.1f} "
               f"start {(x[1]-t0)/1e3:7.1f} end {(x[2]-t0)/1e3:7.1f} us")
+
+# aggregate per (src,dst) class
+import collections
+agg = collections.defaultdict(lambda: np.zeros(6))
+cnt = collections.Counter()
+for rr in r:
+    key = (["ring","glob","flag"][(int(rr[0]) >> 32) & 0xff], ["ring","glob","flag"][(int(rr[0]) >> 40) & 0xff])
+    agg[key] += rr[3:9]; cnt[key] += 1
+for key, v in sorted(agg.items()):
+    print(f"  {key[0]:>4s}->{key[1]:<4s} n={cnt[key]:5d}: " + ", ".join(f"{a} {100*x/v.sum():.1f}%" for a, x in zip(names, v)))
