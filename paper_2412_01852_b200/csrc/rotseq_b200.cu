@@ -39,6 +39,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "rotseq_b200.h"
 
@@ -272,6 +273,8 @@ struct PipeParams {
   int nblk;              // nchunk + 1
   int nw;                // warps per CTA
   int debug_no_chain;    // timing experiments only: every unit reads/writes A (wrong result)
+  int debug_mode;        // timing experiments only (wrong result): 1 = no I/O or ring waits,
+                         // 2 = no coefficient staging, 3 = both
   int smsp_group;        // place chain neighbours on the same SM sub-partition
   int elastic;           // rings only within a sub-partition group, flags across
 };
@@ -364,17 +367,17 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
-  // Position of this warp inside a round. Chain neighbours (positions q, q+1) are placed
-  // on the same SM sub-partition (warp id mod 4) when smsp_group is set, so a consumer that
-  // waits for its producer yields the FP64 pipe to exactly that producer.
-  int qpos = warp;
-  if (P.smsp_group) {
-    // Balance the positions actually used in the first round (n_eff <= NW) over the four
-    // sub-partitions (e.g. 10 units -> 3,3,2,2 rather than 3,3,3,1); idle warps take the
-    // remaining positions.
-    const long long U0 = P.units * (long long)blockIdx.x / gridDim.x;
-    const long long U1 = P.units * (long long)(blockIdx.x + 1) / gridDim.x;
-    const int n_eff = (int)min((long long)NW, U1 - U0);
+  const int lane = threadIdx.x & 31;
+  const long long U = P.units;
+  const long long G = gridDim.x;
+  const long long ub = U * (long long)blockIdx.x / G;
+  const long long ue = U * (long long)(blockIdx.x + 1) / G;
+  // Position of this warp inside a round: chain neighbours (positions q, q+1) share an SM
+  // sub-partition (warp id mod 4), and the positions used in the first round are balanced
+  // over the four sub-partitions (10 units -> 3,3,2,2); idle warps take the rest.
+  int qpos;
+  {
+    const int n_eff = (int)min((long long)NW, ue - ub);
     const int sub = warp & 3, idx = warp >> 2;
     int act_start = 0, idle_start = 0;
     for (int s2 = 0; s2 < sub; ++s2) {
@@ -383,29 +386,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       idle_start += (NW - s2 + 3) / 4 - c;
     }
     const int c_sub = (n_eff - sub + 3) / 4;
-    // the warp scheduler favours higher warp ids; with smsp_group == 2 the upstream
-    // (producer) end of each group gets the highest id so rings stay filled
-    const int idx2 = (P.smsp_group == 2 && idx < c_sub) ? c_sub - 1 - idx : idx;
-    qpos = idx2 < c_sub ? act_start + idx2 : n_eff + idle_start + (idx2 - c_sub);
+    qpos = idx < c_sub ? act_start + idx : n_eff + idle_start + (idx - c_sub);
   }
-  // Sub-partition group of a position (positions of one group share an SMSP). With
-  // P.elastic, ring hand-offs are kept only inside a group; across groups the chain goes
-  // through A + progress flags, whose unbounded slack lets every SMSP run at its own pace.
-  auto group_of = [&](int q) -> int {
-    if (!P.smsp_group) return q;
-    const long long U0 = P.units * (long long)blockIdx.x / gridDim.x;
-    const long long U1 = P.units * (long long)(blockIdx.x + 1) / gridDim.x;
-    const int n_eff = (int)min((long long)NW, U1 - U0);
-    int start = 0;
-    for (int s2 = 0; s2 < 4; ++s2) {
-      start += (n_eff - s2 + 3) / 4;
-      if (q < start) return s2;
-    }
-    return 4 + q;
-  };
-  const bool ring_from_prev = qpos > 0 && (!P.elastic || group_of(qpos - 1) == group_of(qpos));
-  const bool ring_to_next = qpos < NW - 1 && (!P.elastic || group_of(qpos) == group_of(qpos + 1));
-  const int lane = threadIdx.x & 31;
   CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);
   T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * CBLK);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
@@ -420,20 +402,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   }
   __syncthreads();
 
-  const long long U = P.units;
-  const long long G = gridDim.x;
-  const long long ub = U * (long long)blockIdx.x / G;
-  const long long ue = U * (long long)(blockIdx.x + 1) / G;
-
   T* const A = reinterpret_cast<T*>(P.A);
   const int len = P.len;
   const int nchunk = P.nchunk;
   const int nblk = P.nblk;
-  uint64_t* const bar_in = bars + qpos * NBAR;             // full_in[S], consumed, coef[2]
+  const int bands = P.bands;
+  uint64_t* const bar_in = bars + qpos * NBAR;  // full_in[S], consumed, coef[2]
   uint64_t* const full_in = bar_in;
   uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
   uint64_t* const cbar = bar_in + S + 1;
-  uint64_t* const full_out = bars + (qpos + 1) * NBAR;      // next warp's ring (only with DST_RING)
+  uint64_t* const full_out = bars + (qpos + 1) * NBAR;  // next position's ring (only with DST_RING)
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)qpos * S * CHUNK;
   T* const rout = ring_sm + (size_t)(qpos + 1) * S * CHUNK;
@@ -443,7 +421,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   // Processing order inside the CTA: when the range ends in a partial tile (its low bands
   // feed the next CTA), run that tail first so the next CTA's start never waits for this
   // CTA's last round; the rest follows in natural tile-major order.
-  const int bands = P.bands;
   const long long tail_start = (ue / bands) * bands;
   const bool reorder = (ue % bands != 0) && (tail_start > ub);
   const long long ntail = reorder ? ue - tail_start : 0;
@@ -465,14 +442,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     const int Kb = min(K, P.k - band * K);
     // producer of u is u-1, consumer is u+1 (same tile); ring hand-off only when they are
     // adjacent positions of the same round of this CTA, else through A + progress flag.
-    int src = band == 0 ? SRC_GLOBAL
-                        : ((ring_from_prev && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
-    int dst = band == bands - 1 ? DST_GLOBAL
-                                : ((ring_to_next && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
-    if (P.debug_no_chain) {
-      src = SRC_GLOBAL;
-      dst = DST_GLOBAL;
-    }
+    const int src = band == 0 ? SRC_GLOBAL
+                              : ((qpos > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
+    const int dst = band == bands - 1
+                        ? DST_GLOBAL
+                        : ((qpos < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
+    const bool self = src != SRC_RING;
 
     T* grow[R];        // element (row r, column 0) of this lane's lines
     long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
@@ -486,14 +461,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     const CoefT* csrc = reinterpret_cast<const CoefT*>(P.coef) + (size_t)band * nblk * CBLK;
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
     const uint32_t* myflag = P.flags + u;
+    uint32_t* const outflag = P.flags + u + 1;
 
     // coefficient block 0 of this unit
     if (lane == 0) bulk_g2s(cbuf + (cseq & 1) * CBLK, csrc, kCoefBytes, &cbar[cseq & 1]);
 
     // self-filled input (band 0 reads A; a hand-off reads A after the producer's flag):
-    // cp.async (LDGSTS) straight into this warp's own ring slot, no staging registers.
-    // The slot of chunk q was last used by chunk q-S, consumed by this warp already.
-    uint32_t flag_seen = 0;  // last progress value read (poll only when it is not enough)
+    // cp.async (LDGSTS) straight into this warp's own ring slot, two chunks ahead.
+    uint32_t flag_seen = 0;
     auto fill_chunk = [&](int q) {
       if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
       T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
@@ -523,8 +498,306 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       }
       cp_async_commit();
     };
-    // chunk q is published once its cp.async group completed; one younger group (q+1)
-    // may still be in flight (two-chunk-ahead prefetch: slot of q+2 = slot of q-1)
+    // Self-filled chunks still arrive on full_in (nobody waits on them) so the barrier's
+    // phase count stays equal to the chunk sequence number for ring-fed rounds later on.
+    if (self) {
+      fill_chunk(0);
+      if (1 < nchunk) fill_chunk(1);
+      if (1 < nchunk)
+        cp_async_wait_group<1>();
+      else
+        cp_async_wait_group<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_in[seq0 % S]);
+    }
+
+    T w[R][K + 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) w[r][s] = T(0);
+
+    const int full_hi = (Kb == K && len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
+
+    // One block: protocol + compute. EDGE / OUTRING are compile-time so the interior loop
+    // carries no per-block branches beyond the hand-off protocol of this unit.
+    auto block = [&](int b, auto edge_c, auto outring_c) {
+      constexpr bool EDGE = decltype(edge_c)::value;
+      constexpr bool OUTRING = decltype(outring_c)::value;
+      if (lane == 0 && b + 1 < nblk)
+        bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes, &cbar[(cseq + 1) & 1]);
+      const bool has_in = !EDGE || b < nchunk;
+      const bool has_out = !EDGE || b >= 1;
+      if (self && b + 2 < nchunk) fill_chunk(b + 2);
+      const uint32_t iseq = seq0 + (uint32_t)b;
+      const T* islot = rin + (iseq % S) * CHUNK;
+      const uint32_t oseq = seq0 + (uint32_t)b - 1u;
+      T* oslot = rout + (oseq % S) * CHUNK;
+      mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
+      if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+      if (OUTRING && has_out && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
+      run_block<T, K, R, STRICT, REFL, EDGE, OUTRING>(w, cbuf + (cseq & 1) * CBLK, islot, oslot, grow, gcs, b, len,
+                                                      Kb, lane, b < nchunk, b >= 1);
+      __syncwarp();
+      if (lane == 0) {
+        if (has_in) st_release_shared(consumed_in, iseq + 1u);
+        if (OUTRING && has_out) mbar_arrive(&full_out[oseq % S]);
+        if (dst == DST_FLAG && has_out && ((b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
+          // the warp barrier above orders every lane's stores before lane 0's gpu-scope
+          // fence; the release store then publishes "chunks 0..b-1 are in A"
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          st_release(outflag, (uint32_t)b);
+        }
+      }
+      if (self && b + 1 < nchunk) {  // the chunk read by the next block has landed
+        if (b + 2 < nchunk)
+          cp_async_wait_group<1>();
+        else
+          cp_async_wait_group<0>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full_in[(iseq + 1u) % S]);
+      }
+      ++cseq;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
+    if (dst == DST_RING) {
+      block(0, T_{}, T_{});
+      for (int b = 1; b < interior_end; ++b) block(b, F_{}, T_{});
+      for (int b = max(1, interior_end); b < nblk; ++b) block(b, T_{}, T_{});
+    } else {
+      block(0, T_{}, F_{});
+      for (int b = 1; b < interior_end; ++b) block(b, F_{}, F_{});
+      for (int b = max(1, interior_end); b < nblk; ++b) block(b, T_{}, F_{});
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// v2: lock-step band groups inside a warp ("group pipeline")
+//   A warp runs G consecutive bands of one tile of TR = (32/G)*R owners: lane group g
+//   (lanes g*32/G ..) applies band bg*G+g to the same TR rows. Group g processes block
+//   b-g at step b, so the column group g emits at wave u is exactly the column group g+1
+//   loads at the same wave: it moves with shfl.up (no waiting, no shared memory). Only
+//   group 0's input and group G-1's output go through rings / A, so a tile's chain has
+//   bands/G - 1 inter-warp links instead of bands - 1.
+// ------------------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T shfl_up_t(T v, int d) {
+  return __shfl_up_sync(0xffffffffu, v, d);
+}
+
+template <typename T, int K, int R, int G, bool STRICT, bool REFL, bool EDGE, bool OUTRING>
+__device__ __forceinline__ void gp_step(T (&w)[R][K + 1], const Coef<T, REFL>* __restrict__ cb,
+                                        const T* __restrict__ islot, T* __restrict__ oslot,
+                                        T* const (&gout)[R], const long long (&gcs)[R], int b, int len, int nblk,
+                                        int grp, int Kb, int sl, bool in_ok, bool out_ok) {
+  constexpr int LPG = 32 / G;
+  constexpr int TR = LPG * R;
+  const int gb = b - grp;  // this lane group's block
+  const bool gact = !EDGE || (gb >= 0 && gb < nblk);
+  const long long c0 = (long long)gb * (K + 1);
+  const long long ic0 = (long long)b * (K + 1);        // group 0's input columns
+  const long long oc0 = (long long)(b - G) * (K + 1);  // group G-1's output columns
+  const bool last = grp == G - 1;
+  const bool first = grp == 0;
+  T* gp[R];
+  if constexpr (!OUTRING) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) gp[r] = gout[r] + oc0 * gcs[r];
+  }
+#pragma unroll
+  for (int u = 0; u <= K; ++u) {
+    T e[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) e[r] = w[r][u];
+    // group G-1 emits column (b-G)(K+1)+u to the next warp / A
+    if (last && (!EDGE || (out_ok && oc0 + u < len))) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if constexpr (OUTRING)
+          oslot[u * TR + sl + LPG * r] = e[r];
+        else
+          *gp[r] = e[r];
+      }
+    }
+    if constexpr (!OUTRING) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) gp[r] += gcs[r];
+    }
+    // group g > 0 takes group g-1's emitted column; group 0 reads the ring
+    T v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = shfl_up_t(e[r], LPG);
+    if (first) {
+      if (!EDGE || (in_ok && ic0 + u < len)) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = islot[u * TR + sl + LPG * r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = T(0);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) w[r][u] = v[r];
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+      constexpr int M = K + 1;
+      const int sx = (u - 1 - l + 2 * M) % M;
+      const int sy = (sx + 1) % M;
+      const Coef<T, REFL> cf = cb[(u * K + l) * G];
+      if constexpr (EDGE) {
+        const long long j = c0 + u - 1 - l;
+        const bool valid = gact && l < Kb && j >= 0 && j <= (long long)len - 2;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          T x = w[r][sx], y = w[r][sy];
+          xform<T, STRICT, REFL>(x, y, cf);
+          w[r][sx] = valid ? x : w[r][sx];
+          w[r][sy] = valid ? y : w[r][sy];
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+      }
+    }
+  }
+}
+
+template <typename T, int K, int R, int G, bool STRICT, bool REFL>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_gpipe_kernel(const __grid_constant__ PipeParams P) {
+  using CoefT = Coef<T, REFL>;
+  constexpr int LPG = 32 / G;
+  constexpr int TR = LPG * R;          // owners per tile
+  constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
+  constexpr int CBLK = (K + 1) * K;
+  constexpr int S = kStages;
+  constexpr int NBAR = kCtlWords;
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NW = P.nw;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int grp = lane / LPG;
+  const int sl = lane - grp * LPG;
+  CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);                       // [NW][2][G][CBLK]
+  T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * G * CBLK);   // [NW][S][CHUNK]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
+  if (threadIdx.x < NW) {
+    uint64_t* bw = bars + threadIdx.x * NBAR;
+#pragma unroll
+    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
+    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
+    mbar_init(bw + S + 1, 1);
+    mbar_init(bw + S + 2, 1);
+  }
+  __syncthreads();
+
+  const long long U = P.units;
+  const long long Gr = gridDim.x;
+  const long long ub = U * (long long)blockIdx.x / Gr;
+  const long long ue = U * (long long)(blockIdx.x + 1) / Gr;
+  // chain neighbours on the same SM sub-partition, balanced over the four (see v1)
+  int qpos = warp;
+  {
+    const int n_eff = (int)min((long long)NW, ue - ub);
+    const int sub = warp & 3, idx = warp >> 2;
+    int act_start = 0, idle_start = 0;
+    for (int s2 = 0; s2 < sub; ++s2) {
+      const int c = (n_eff - s2 + 3) / 4;
+      act_start += c;
+      idle_start += (NW - s2 + 3) / 4 - c;
+    }
+    const int c_sub = (n_eff - sub + 3) / 4;
+    qpos = idx < c_sub ? act_start + idx : n_eff + idle_start + (idx - c_sub);
+  }
+
+  T* const A = reinterpret_cast<T*>(P.A);
+  const int len = P.len;
+  const int nchunk = P.nchunk;
+  const int nblk = P.nblk;
+  const int nsteps = nblk + G - 1;
+  const int bgroups = (P.bands + G - 1) / G;
+  uint64_t* const bar_in = bars + qpos * NBAR;
+  uint64_t* const full_in = bar_in;
+  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
+  uint64_t* const cbar = bar_in + S + 1;
+  uint64_t* const full_out = bars + (qpos + 1) * NBAR;
+  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
+  T* const rin = ring_sm + (size_t)qpos * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(qpos + 1) * S * CHUNK;
+  CoefT* const cbuf = coef_sm + (size_t)qpos * 2 * G * CBLK;
+  constexpr uint32_t kCoefBytes = (uint32_t)(CBLK * sizeof(CoefT));
+
+  const long long tail_start = (ue / bgroups) * bgroups;
+  const bool reorder = (ue % bgroups != 0) && (tail_start > ub);
+  const long long ntail = reorder ? ue - tail_start : 0;
+  auto unit_at = [&](long long p) -> long long {
+    return reorder ? (p < ntail ? tail_start + p : ub + (p - ntail)) : ub + p;
+  };
+  auto pos_of = [&](long long uu) -> long long {
+    return reorder ? (uu >= tail_start ? uu - tail_start : uu - ub + ntail) : uu - ub;
+  };
+
+  uint32_t cseq = 0;
+  for (int jr = 0;; ++jr) {
+    const long long p = (long long)jr * NW + qpos;
+    if (p >= ue - ub) break;
+    const long long u = unit_at(p);
+    const long long tile = u / bgroups;
+    const int bgi = (int)(u - tile * bgroups);
+    const int band0 = bgi * G;
+    const int myband = band0 + grp;
+    const int Kb = myband < P.bands ? min(K, P.k - myband * K) : 0;
+    int src = bgi == 0 ? SRC_GLOBAL : ((qpos > 0 && u - 1 >= ub && pos_of(u - 1) == p - 1) ? SRC_RING : SRC_FLAG);
+    int dst = bgi == bgroups - 1 ? DST_GLOBAL
+                                 : ((qpos < NW - 1 && u + 1 < ue && pos_of(u + 1) == p + 1) ? DST_RING : DST_FLAG);
+    // every group is a full band of K sweeps and every band exists -> interior steps allowed
+    const bool all_full = (band0 + G <= P.bands) && (P.k - (band0 + G - 1) * K >= K);
+
+    // per-lane row pointers: group 0 lanes read A (self-fill), group G-1 lanes write A
+    T* grow[R];
+    long long gcs[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long o = tile * TR + sl + LPG * r;
+      const bool ok = o < P.owners;
+      grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
+      gcs[r] = ok ? P.cs : 0;
+    }
+    const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
+    const uint32_t* myflag = P.flags + u;
+
+    const int nsteps_pack = nblk + G - 1;
+    const CoefT* csrc = reinterpret_cast<const CoefT*>(P.coef) + (size_t)bgi * nsteps_pack * G * CBLK;
+    auto issue_coef = [&](int step, uint32_t buf) {
+      if (lane == 0)
+        bulk_g2s(cbuf + (size_t)buf * G * CBLK, csrc + (size_t)step * G * CBLK, G * kCoefBytes, &cbar[buf]);
+    };
+    issue_coef(0, cseq & 1);
+
+    uint32_t flag_seen = 0;
+    auto fill_chunk = [&](int q) {
+      if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
+      T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
+      if (grp == 0) {
+        const long long c0 = (long long)q * (K + 1);
+        const T* sp[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) sp[r] = grow[r] + c0 * gcs[r];
+#pragma unroll
+        for (int v = 0; v <= K; ++v) {
+          const bool cv = c0 + v < len;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            cp_async_elem(dstp + v * TR + sl + LPG * r, cv ? sp[r] : grow[r], cv);
+            sp[r] += gcs[r];
+          }
+        }
+      }
+      cp_async_commit();
+    };
     auto publish_chunk = [&](int q, bool younger_in_flight) {
       if (younger_in_flight)
         cp_async_wait_group<1>();
@@ -533,9 +806,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_in[(seq0 + (uint32_t)q) % S]);
     };
-    TraceAcc tacc;
-    tacc.t0 = trace_gtime();
-    unsigned long long tc = trace_clock();
     if (src != SRC_RING) {
       fill_chunk(0);
       if (1 < nchunk) fill_chunk(1);
@@ -546,80 +816,56 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int s = 0; s <= K; ++s) w[r][s] = T(0);
+      for (int s2 = 0; s2 <= K; ++s2) w[r][s2] = T(0);
 
-    const bool full_band = (Kb == K);
-    const int full_hi = (full_band && len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
+    const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
 
-    for (int b = 0; b < nblk; ++b) {
-      if (lane == 0 && b + 1 < nblk)
-        bulk_g2s(cbuf + ((cseq + 1) & 1) * CBLK, csrc + (size_t)(b + 1) * CBLK, kCoefBytes,
-                 &cbar[(cseq + 1) & 1]);
+    for (int b = 0; b < nsteps; ++b) {
+      if (b + 1 < nsteps) issue_coef(b + 1, (cseq + 1) & 1);
       const bool self_next = (src != SRC_RING) && (b + 1 < nchunk);
       const bool self_next2 = (src != SRC_RING) && (b + 2 < nchunk);
-      tc = trace_clock();
       if (self_next2) fill_chunk(b + 2);
-      unsigned long long tn = trace_clock();
-      tacc.c[0] += tn - tc;
-      tc = tn;
 
       mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
-      tn = trace_clock();
-      tacc.c[1] += tn - tc;
-      tc = tn;
-      const bool has_in = b < nchunk;
-      const bool has_out = b >= 1;
+      const bool in_ok = b < nchunk;
+      const int oq = b - G;  // output chunk of this step
+      const bool out_ok = oq >= 0 && oq < nchunk;
       const uint32_t iseq = seq0 + (uint32_t)b;
       const T* islot = rin + (iseq % S) * CHUNK;
-      if (has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
-      tn = trace_clock();
-      tacc.c[2] += tn - tc;
-      tc = tn;
-      const uint32_t oseq = seq0 + (uint32_t)b - 1u;
+      if (in_ok) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+      const uint32_t oseq = seq0 + (uint32_t)oq;
       T* oslot = rout + (oseq % S) * CHUNK;
-      if (dst == DST_RING && has_out && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
+      if (dst == DST_RING && out_ok && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
 
-      tn = trace_clock();
-      tacc.c[3] += tn - tc;
-      tc = tn;
-      const CoefT* cb = cbuf + (cseq & 1) * CBLK;
-      const bool interior = b >= 1 && b <= full_hi;
+      const CoefT* cb = cbuf + (size_t)(cseq & 1) * G * CBLK + grp;  // record (u,l) at cb[(u*K+l)*G]
+      const bool interior = all_full && b >= G && b <= full_hi;
       if (interior) {
         if (dst == DST_RING)
-          run_block<T, K, R, STRICT, REFL, false, true>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
-                                                        has_in, has_out);
+          gp_step<T, K, R, G, STRICT, REFL, false, true>(w, cb, islot, oslot, grow, gcs, b, len, nblk, grp, Kb, sl,
+                                                          in_ok, out_ok);
         else
-          run_block<T, K, R, STRICT, REFL, false, false>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
-                                                         has_in, has_out);
+          gp_step<T, K, R, G, STRICT, REFL, false, false>(w, cb, islot, oslot, grow, gcs, b, len, nblk, grp, Kb, sl,
+                                                           in_ok, out_ok);
       } else {
         if (dst == DST_RING)
-          run_block<T, K, R, STRICT, REFL, true, true>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
-                                                       has_in, has_out);
+          gp_step<T, K, R, G, STRICT, REFL, true, true>(w, cb, islot, oslot, grow, gcs, b, len, nblk, grp, Kb, sl,
+                                                         in_ok, out_ok);
         else
-          run_block<T, K, R, STRICT, REFL, true, false>(w, cb, islot, oslot, grow, gcs, b, len, Kb, lane,
-                                                        has_in, has_out);
+          gp_step<T, K, R, G, STRICT, REFL, true, false>(w, cb, islot, oslot, grow, gcs, b, len, nblk, grp, Kb, sl,
+                                                          in_ok, out_ok);
       }
       __syncwarp();
-      tn = trace_clock();
-      tacc.c[4] += tn - tc;
-      tc = tn;
       if (lane == 0) {
-        if (has_in) st_release_shared(consumed_in, iseq + 1u);
-        if (dst == DST_RING && has_out) mbar_arrive(&full_out[oseq % S]);
+        if (in_ok) st_release_shared(consumed_in, iseq + 1u);
+        if (dst == DST_RING && out_ok) mbar_arrive(&full_out[oseq % S]);
       }
-      if (dst == DST_FLAG && has_out && lane == 0 && ((b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
-        // the warp barrier above orders every lane's stores before lane 0's gpu-scope
-        // fence; the release store then publishes "chunks 0..b-1 are in A"
+      if (dst == DST_FLAG && out_ok && lane == 0 && ((oq & (kFlagEvery - 1)) == 0 || oq == nchunk - 1)) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        st_release(P.flags + u + 1, (uint32_t)b);
+        st_release(P.flags + u + 1, (uint32_t)(oq + 1));
       }
       if (self_next) publish_chunk(b + 1, self_next2);
       ++cseq;
-      tn = trace_clock();
-      tacc.c[5] += tn - tc;
-      tc = tn;
     }
-    trace_unit(warp, jr, u, src, dst, tacc, nblk);
   }
 }
 
@@ -648,6 +894,60 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
     const int j = b * (K + 1) + u - 1 - l;
     Coef<T, REFL> cf;
     if (p < k && j >= 0 && j <= len - 2) {
+      const long long jj = rev ? (long long)(len - 2 - j) : (long long)j;
+      T c = __ldg(C + jj + (long long)p * ldcs);
+      T s = __ldg(Sm + jj + (long long)p * ldcs);
+      if constexpr (REFL) {
+        if (rev) c = -c;
+        cf.s = s;
+        cf.d = c - s;
+        cf.e = c + s;
+        cf.pad = T(0);
+      } else {
+        if (rev) s = -s;
+        cf.c = c;
+        cf.s = s;
+      }
+    } else {
+      if constexpr (REFL) {
+        cf.s = T(0);
+        cf.d = T(0);
+        cf.e = T(0);
+        cf.pad = T(0);
+      } else {
+        cf.c = T(0);
+        cf.s = T(0);
+      }
+    }
+    dst[i] = cf;
+  }
+}
+
+// Group-pipeline layout: [band group][step][u][l][g] — at step b lane group g needs block
+// b-g of band bg*G+g, so one contiguous bulk copy per step serves all groups and the G
+// records a warp reads for (u, l) are adjacent (one 16*G-byte segment per LDS.128).
+template <typename T, int K, int G, bool REFL>
+__global__ void __launch_bounds__(256) rs_pack_g_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
+                                                        const T* __restrict__ Sm, long long ldcs, int len, int k,
+                                                        int bands, int nblk, int rev) {
+  constexpr int E = (K + 1) * K * G;
+  const int bg = blockIdx.y;
+  const int nsteps = nblk + G - 1;
+  const int total = nsteps * E;
+  Coef<T, REFL>* dst = out + (size_t)bg * total;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int step = i / E;
+    int e = i - step * E;
+    const int u = e / (K * G);
+    e -= u * (K * G);
+    const int l = e / G;
+    const int g = e - l * G;
+    const int band = bg * G + g;
+    const int blk = step - g;
+    const int p = band * K + l;
+    const int j = blk * (K + 1) + u - 1 - l;
+    Coef<T, REFL> cf;
+    if (band < bands && blk >= 0 && blk < nblk && p < k && j >= 0 && j <= len - 2) {
       const long long jj = rev ? (long long)(len - 2 - j) : (long long)j;
       T c = __ldg(C + jj + (long long)p * ldcs);
       T s = __ldg(Sm + jj + (long long)p * ldcs);
@@ -723,6 +1023,8 @@ struct Geometry {
   size_t coef_bytes = 0;
   size_t flag_bytes = 0;
   size_t coef_rec = 0;
+  long long units_g2 = 0;  // v2 group pipeline, G = 2 (tiles of 32 owners)
+  long long units_g4 = 0;  // v2 group pipeline, G = 4 (tiles of 16 owners)
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -741,8 +1043,21 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   g->nblk = g->nchunk + 1;
   const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
   g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 : 2) * tsz;
-  g->coef_bytes = align_up((size_t)g->bands * g->nblk * (kK + 1) * kK * g->coef_rec, 256);
-  g->flag_bytes = align_up((size_t)(g->units + 1) * sizeof(uint32_t), 256) + kTrashBytes;
+  {
+    const size_t per_rec = (size_t)(kK + 1) * kK * g->coef_rec;
+    size_t v1 = (size_t)g->bands * g->nblk * per_rec;
+    size_t g2 = (size_t)((g->bands + 1) / 2) * (g->nblk + 1) * 2 * per_rec;
+    size_t g4 = (size_t)((g->bands + 3) / 4) * (g->nblk + 3) * 4 * per_rec;
+    size_t mx = v1 > g2 ? v1 : g2;
+    if (g4 > mx) mx = g4;
+    g->coef_bytes = align_up(mx, 256);
+  }
+  g->units_g2 = ((g->owners + 16 * kR - 1) / (16 * kR)) * ((g->bands + 1) / 2);
+  g->units_g4 = ((g->owners + 8 * kR - 1) / (8 * kR)) * ((g->bands + 3) / 4);
+  long long umax = g->units;
+  if (g->units_g2 > umax) umax = g->units_g2;
+  if (g->units_g4 > umax) umax = g->units_g4;
+  g->flag_bytes = align_up((size_t)(umax + 1) * sizeof(uint32_t), 256) + kTrashBytes;
   return true;
 }
 
@@ -750,22 +1065,44 @@ struct LaunchPlan {
   int grid = 0;
   int nw = 0;
   size_t smem = 0;
+  long long units = 0;
+  int variant = 0;
 };
 
-size_t smem_per_warp(size_t tsz, size_t coef_rec) {
-  return 2 * (size_t)(kK + 1) * kK * coef_rec + (size_t)kStages * (kK + 1) * kTileOwners * tsz +
-         kCtlWords * sizeof(uint64_t);
+// kernel variants: v1 = one band per warp; g2 / g4 = lock-step groups of 2 / 4 bands
+enum : int { VAR_V1 = 0, VAR_G2 = 2, VAR_G4 = 4 };
+
+int kernel_variant() {
+  const char* e = getenv("RS_KERNEL");
+  if (e == nullptr) return VAR_G4;
+  if (strcmp(e, "v1") == 0) return VAR_V1;
+  if (strcmp(e, "g2") == 0) return VAR_G2;
+  return VAR_G4;
 }
 
-rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
+size_t smem_per_warp(size_t tsz, size_t coef_rec, int variant) {
+  const size_t cblk = (size_t)(kK + 1) * kK * coef_rec;
+  if (variant == VAR_V1)
+    return 2 * cblk + (size_t)kStages * (kK + 1) * kTileOwners * tsz + kCtlWords * sizeof(uint64_t);
+  const size_t groups = (size_t)variant;
+  const size_t tile = (size_t)(32 / variant) * kR;
+  return 2 * groups * cblk + (size_t)kStages * (kK + 1) * tile * tsz + kCtlWords * sizeof(uint64_t);
+}
+
+long long variant_units(const Geometry& g, int variant) {
+  return variant == VAR_V1 ? g.units : (variant == VAR_G2 ? g.units_g2 : g.units_g4);
+}
+
+rs_status plan_launch(const Geometry& g, size_t tsz, int variant, LaunchPlan* lp) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(RS_ECUDA, "cudaGetDevice failed");
   int sms = 0, optin = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
-  const size_t per = smem_per_warp(tsz, g.coef_rec);
-  // one extra barrier block for the (never used) ring of warp nw
+  const size_t per = smem_per_warp(tsz, g.coef_rec, variant);
+  const long long units = variant_units(g, variant);
+  // one extra control block for the (never used) ring of warp nw
   int cap = (int)((optin - kCtlWords * sizeof(uint64_t)) / per);
   if (cap > kMaxWarps) cap = kMaxWarps;
   if (cap < 1) return fail(RS_EUNSUPPORTED, "shared memory too small for one pipeline warp");
@@ -779,9 +1116,9 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     const long long v = atoll(ev);
     if (v >= 1 && v < grid) grid = v;
   }
-  if (g.units < grid) grid = g.units;
+  if (units < grid) grid = units;
   if (grid < 1) grid = 1;
-  const double x = (double)g.units / (double)grid;
+  const double x = (double)units / (double)grid;
   // units per CTA x: one round of ceil(x) warps when it fits, else the fewest rounds of
   // at most `cap` warps, spread evenly so the last round is as full as possible.
   long long rounds = (long long)ceil(x / cap);
@@ -792,6 +1129,8 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   lp->grid = (int)grid;
   lp->nw = nw;
   lp->smem = per * nw + kCtlWords * sizeof(uint64_t);
+  lp->units = units;
+  lp->variant = variant;
   return RS_OK;
 }
 
@@ -800,11 +1139,24 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
                       cudaStream_t st) {
   using CoefT = Coef<T, REFL>;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
-  const int per_band = g.nblk * (kK + 1) * kK;
-  int bx = (per_band + 255) / 256;
-  if (bx > 64) bx = 64;
-  dim3 pgrid((unsigned)bx, (unsigned)g.bands);
-  rs_pack_kernel<T, kK, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk, rev);
+  const int variant = kernel_variant();
+  if (variant == VAR_V1) {
+    const int per_band = g.nblk * (kK + 1) * kK;
+    int bx = (per_band + 255) / 256;
+    if (bx > 64) bx = 64;
+    dim3 pgrid((unsigned)bx, (unsigned)g.bands);
+    rs_pack_kernel<T, kK, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk, rev);
+  } else {
+    const int G = variant;
+    const int per_group = (g.nblk + G - 1) * (kK + 1) * kK * G;
+    int bx = (per_group + 255) / 256;
+    if (bx > 128) bx = 128;
+    dim3 pgrid((unsigned)bx, (unsigned)((g.bands + G - 1) / G));
+    if (G == 2)
+      rs_pack_g_kernel<T, kK, 2, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.bands, g.nblk, rev);
+    else
+      rs_pack_g_kernel<T, kK, 4, REFL><<<pgrid, 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.bands, g.nblk, rev);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
@@ -817,7 +1169,7 @@ template <typename T, bool STRICT, bool REFL>
 rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st) {
   using CoefT = Coef<T, REFL>;
   LaunchPlan lp;
-  rs_status rc = plan_launch(g, sizeof(T), &lp);
+  rs_status rc = plan_launch(g, sizeof(T), kernel_variant(), &lp);
   if (rc != RS_OK) return rc;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
   uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes);
@@ -829,7 +1181,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.cs = rev ? -g.cs : g.cs;
   if (rev) P.A = Abase + (long long)(g.len - 1) * g.cs;
   P.owners = g.owners;
-  P.units = g.units;
+  P.units = lp.units;
   P.coef = coef;
   P.flags = flags;
   P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flag_bytes - kTrashBytes;
@@ -840,21 +1192,25 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.nblk = g.nblk;
   P.nw = lp.nw;
   P.debug_no_chain = getenv("RS_DEBUG_NO_CHAIN") ? atoi(getenv("RS_DEBUG_NO_CHAIN")) : 0;
+  P.debug_mode = getenv("RS_DEBUG_MODE") ? atoi(getenv("RS_DEBUG_MODE")) : 0;
   P.smsp_group = getenv("RS_SMSP_GROUP") ? atoi(getenv("RS_SMSP_GROUP")) : 1;
   P.elastic = getenv("RS_ELASTIC") ? atoi(getenv("RS_ELASTIC")) : 0;
-  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL>;
+  auto kern = lp.variant == VAR_V1   ? rs_pipeline_kernel<T, kK, kR, STRICT, REFL>
+              : lp.variant == VAR_G2 ? rs_gpipe_kernel<T, kK, kR, 2, STRICT, REFL>
+                                     : rs_gpipe_kernel<T, kK, kR, 4, STRICT, REFL>;
   {
     // opt in to the large dynamic shared memory once per (kernel, device)
-    static std::atomic<int> configured_mask{0};
+    static std::atomic<int> configured_mask[3] = {{0}, {0}, {0}};
+    std::atomic<int>& configured = configured_mask[lp.variant == VAR_V1 ? 0 : (lp.variant == VAR_G2 ? 1 : 2)];
     int dev = 0;
     cudaGetDevice(&dev);
     const int bit = 1 << (dev & 31);
-    if (!(configured_mask.load(std::memory_order_relaxed) & bit)) {
+    if (!(configured.load(std::memory_order_relaxed) & bit)) {
       int optin = 0;
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
       if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-      configured_mask.fetch_or(bit, std::memory_order_relaxed);
+      configured.fetch_or(bit, std::memory_order_relaxed);
     }
   }
   cudaLaunchConfig_t cfg = {};
@@ -1115,13 +1471,13 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
   Geometry g;
   make_geometry(m, n, m > 1 ? m : 1, k, side, kind, dtype, &g);
   LaunchPlan lp;
-  rs_status rc = plan_launch(g, dtype == RS_DTYPE_F64 ? 8 : 4, &lp);
+  rs_status rc = plan_launch(g, dtype == RS_DTYPE_F64 ? 8 : 4, kernel_variant(), &lp);
   if (rc != RS_OK) return rc;
   if (grid_ctas) *grid_ctas = lp.grid;
   if (warps_per_cta) *warps_per_cta = lp.nw;
-  if (units) *units = g.units;
+  if (units) *units = lp.units;
   if (band_width) *band_width = kK;
-  if (rows_per_tile) *rows_per_tile = kTileOwners;
+  if (rows_per_tile) *rows_per_tile = lp.variant == VAR_V1 ? kTileOwners : (32 / lp.variant) * kR;
   if (smem_bytes) *smem_bytes = lp.smem;
   return RS_OK;
 }

@@ -1,5 +1,6 @@
 // FP64 / FP32 pipe microbenchmarks for the roofline denominators (DFMA, FFMA peaks).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 template <typename T, int CH>
 __global__ void fma_tput(T* out, int iters, T a, T b) {
@@ -36,7 +37,18 @@ double run_tput(int blocks, int threads, int iters) {
   cudaFree(o);
   return flops / (ms * 1e-3) / 1e12;
 }
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1) {  // sustained: back-to-back launches for ~N seconds
+    double* o; cudaMalloc(&o, 64);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    int reps = atoi(argv[1]);
+    cudaEventRecord(e0);
+    for (int i = 0; i < reps; ++i) fma_tput<double, 8><<<148 * 8, 256>>>(o, 20000, 0.999, 0.001);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("sustained DFMA over %.1f ms: %.2f TF/s\n", ms, 2.0 * 8 * 20000.0 * 148 * 8 * 256 * reps / (ms * 1e-3) / 1e12);
+    return 0;
+  }
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   printf("device %s SMs %d clock %d kHz\n", p.name, p.multiProcessorCount, p.clockRate);
   int sms = p.multiProcessorCount;
