@@ -33,27 +33,31 @@ print(f"unit start us: min {start.min():.1f} med {np.median(start):.1f} max {sta
 names = ["fill/flag", "coef", "full", "space", "compute", "post"]
 tot = r[:, 3:9].sum(axis=0).astype(float)
 print("cycle shares:", ", ".join(f"{nm} {100*v/tot.sum():.1f}%" for nm, v in zip(names, tot)))
-srcs = (r[:, 0] >> 32) & 0xff
+srcs = (r[:, 0] >> 40) & 0xf
 for sv, nm in ((0, "ring"), (1, "global"), (2, "flag")):
     sel = srcs == sv
     if sel.any():
         t = r[sel, 3:9].sum(axis=0).astype(float)
         print(f"  src={nm:6s} n={sel.sum():5d}:", ", ".join(f"{a} {100*v/t.sum():.1f}%" for a, v in zip(names, t)))
-per_block_compute = r[:, 7].sum() / r[:, 9].sum()
+nblk = (n + 8) // 9 + 1
+kbs = (r[:, 9] >> 32) & 0xff
+per_block_compute = r[:, 7].sum() / (len(r) * nblk)
+print("unit widths:", dict(zip(*np.unique(kbs, return_counts=True))))
 print(f"compute cycles per warp-block: {per_block_compute:.0f}")
 # active units over time (all SMs)
 T = end.max(); bins = np.linspace(0, T, 21)
 act = [((start < b1) & (end > b0)).sum() for b0, b1 in zip(bins[:-1], bins[1:])]
 print("active units per 5% of time:", act)
 # per-warp breakdown for a few CTAs
-print("per-warp (cta,wid,pos,unit,band,src,dst): compute% full% space% flag%  total_cycles")
+print("per-warp (cta,wid,tile,p0,kb,src,dst): compute% full% space% flag%  total_cycles")
 for c in [int(x) for x in os.environ.get("CTAS", "0,1,2,3").split(",")]:
     for w in range(NW):
         x = rec[c, w, 0]
         if x[1] == 0: continue
-        u = int(x[0]) & 0xffffffff; srcv = (int(x[0]) >> 32) & 0xff; dstv = (int(x[0]) >> 40) & 0xff
+        u = int(x[0]) & 0xffffffffff; srcv = (int(x[0]) >> 40) & 0xf; dstv = (int(x[0]) >> 44) & 0xf
+        p0 = int(x[9]) & 0xffffffff; kb = int(x[9]) >> 32
         cyc = x[3:9].astype(float); tt = cyc.sum()
-        print(f"  c{c:3d} w{w:2d} unit {u:5d} band {u % (k // 8):2d} src {['ring','glob','flag'][srcv]} dst {['ring','glob','flag'][dstv]}: "
+        print(f"  c{c:3d} w{w:2d} tile {u:5d} p0 {p0:3d} kb {kb} src {['ring','glob','flag'][srcv]} dst {['ring','glob','flag'][dstv]}: "
               f"comp {100*cyc[4]/tt:5.1f} full {100*cyc[2]/tt:5.1f} space {100*cyc[3]/tt:5.1f} flag {100*cyc[0]/tt:5.1f} "
               f"start {(x[1]-t0)/1e3:7.1f} end {(x[2]-t0)/1e3:7.1f} us")
 
@@ -62,7 +66,9 @@ import collections
 agg = collections.defaultdict(lambda: np.zeros(6))
 cnt = collections.Counter()
 for rr in r:
-    key = (["ring","glob","flag"][(int(rr[0]) >> 32) & 0xff], ["ring","glob","flag"][(int(rr[0]) >> 40) & 0xff])
+    key = (["ring","glob","flag"][(int(rr[0]) >> 40) & 0xf], ["ring","glob","flag"][(int(rr[0]) >> 44) & 0xf])
     agg[key] += rr[3:9]; cnt[key] += 1
 for key, v in sorted(agg.items()):
     print(f"  {key[0]:>4s}->{key[1]:<4s} n={cnt[key]:5d}: " + ", ".join(f"{a} {100*x/v.sum():.1f}%" for a, x in zip(names, v)))
+if os.environ.get("TRACE_SAVE"):
+    np.save(os.environ["TRACE_SAVE"], rec)
