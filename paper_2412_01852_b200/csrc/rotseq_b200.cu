@@ -56,6 +56,9 @@ namespace {
 // ------------------------------------------------------------------------------------
 constexpr int kK = 8;          // max sweeps per unit (lanes of the wavefront)
 constexpr int kR = 2;          // owners (rows) per thread
+#ifndef RS_FLAG_EVERY
+#define RS_FLAG_EVERY 8
+#endif
 #ifndef RS_STAGES
 #define RS_STAGES 2
 #endif
@@ -64,7 +67,7 @@ constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
 constexpr int kTileOwners = 32 * kR;
 constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
 constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
-constexpr int kFlagEvery = 8;   // hand-off progress is published every 8 blocks (fence cost)
+constexpr int kFlagEvery = RS_FLAG_EVERY;   // hand-off progress is published every 8 blocks (fence cost)
 constexpr size_t kTrashBytes = 32 * kR * 8;  // scratch slot per lane for rows past the matrix
 
 enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
@@ -95,6 +98,18 @@ template <typename T>
 struct alignas(4 * sizeof(T)) Coef<T, true> {
   T s, d, e, pad;  // d = c - s, e = c + s (hoisted exactly as core.py:142-143)
 };
+// Scaled ("fast Givens") records: (tau1, -tau2), see rs_pack_scaled_kernel.
+template <typename T>
+using SCoef = Coef<T, false>;
+constexpr int kScaleRecs = 5;  // per block: K+1 = 9 column scales (fp64) in 5 16-byte records
+
+// bytes of one per-warp coefficient buffer (two per warp: double buffering)
+template <typename T, bool REFL>
+__host__ __device__ constexpr size_t coef_buf_bytes() {
+  const size_t std_bytes = (size_t)(kK + 1) * kK * sizeof(Coef<T, REFL>);
+  const size_t scl_bytes = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
+  return std_bytes > scl_bytes ? std_bytes : scl_bytes;
+}
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -131,6 +146,14 @@ __device__ __forceinline__ void refl2(T& x, T& y, T s, T d, T e) {
     x = fma_rn(d, x, w);
     y = fma_rn(-e, y, w);
   }
+}
+// Scaled form (fast mode): the window holds x~ = x / sigma_x per column; one rotation is
+//   x~' = x~ + tau1 * y~ ,  y~' = y~ - tau2 * x~      (2 FMAs instead of 2 MUL + 2 FMA)
+template <typename T>
+__device__ __forceinline__ void xform_scaled(T& x, T& y, const SCoef<T>& cf) {
+  const T xo = x;
+  x = fma_rn(cf.c, y, x);
+  y = fma_rn(cf.s, xo, y);
 }
 template <typename T, bool STRICT, bool REFL>
 __device__ __forceinline__ void xform(T& x, T& y, const Coef<T, REFL>& cf) {
@@ -279,6 +302,8 @@ struct PipeParams {
   long long units;   // U: (tile, sweep-range) units in total
   long long t1;      // the first t1 tiles hold ua+1 units, the others ua
   const void* coef;  // packed coefficient blocks (see rs_pack_kernel)
+  const void* coef_scaled;  // scaled-form blocks (rs_pack_scaled_kernel)
+  const uint32_t* unsafe;   // set by rs_pack_scaled_kernel: scaled form out of safe range
   uint32_t* flags;   // [tiles*k + 1] progress flags of in-place hand-offs, index tile*k + p0
   void* trash;       // 32*R elements: write/read target of lanes past the last row
   int ua;            // units per tile (base)
@@ -287,6 +312,8 @@ struct PipeParams {
   int nchunk;        // ceil(len / (K+1))
   int nblk;          // nchunk + 1
   int nw;            // warps per CTA (multiple of 4)
+  int use_scaled;    // fast fp64: scaled records were packed
+  int credit;        // ring credit in chunks (1..S)
 };
 
 // ------------------------------------------------------------------------------------
@@ -360,8 +387,9 @@ __host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, lon
 //   or to A (global) through one generic store path, so a unit width compiles to ONE loop
 //   body (instruction-cache footprint). EDGE blocks check every column and lane at run time.
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE>
-__device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>* __restrict__ cb,
+template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED>
+__device__ __forceinline__ void run_block(T (&w)[R][K + 1],
+                                          const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* __restrict__ islot, T* const (&op)[R], const long long (&ostr)[R],
                                           int b, int len, int Kb, int lane, bool has_in_rt, bool has_out_rt) {
   constexpr int TR = 32 * R;
@@ -369,6 +397,8 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>*
   const long long c0 = (long long)b * (K + 1);
   const bool has_in = !EDGE || has_in_rt;
   const bool has_out = !EDGE || has_out_rt;
+  // scaled mode: the emitted column is multiplied back by its scale (after the block's records)
+  const T* __restrict__ sc = reinterpret_cast<const T*>(cb + (K + 1) * (EDGE ? Kb : KB));
   T* q[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) q[r] = op[r];
@@ -378,7 +408,13 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>*
       const long long col = c0 - (K + 1) + u;
       if (!EDGE || col < len) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) *q[r] = w[r][u];
+        for (int r = 0; r < R; ++r) {
+          if constexpr (SCALED) {
+            *q[r] = mul_rn(w[r][u], sc[u]);
+          } else {
+            *q[r] = w[r][u];
+          }
+        }
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) q[r] += ostr[r];
@@ -402,9 +438,15 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>*
         const long long j = c0 + u - 1 - l;
         if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
       }
-      const Coef<T, REFL> cf = cb[u * (EDGE ? Kb : KB) + l];
+      const auto cf = cb[u * (EDGE ? Kb : KB) + l];
 #pragma unroll
-      for (int r = 0; r < R; ++r) xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+      for (int r = 0; r < R; ++r) {
+        if constexpr (SCALED) {
+          xform_scaled<T>(w[r][sx], w[r][sy], cf);
+        } else {
+          xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+        }
+      }
     }
   }
 }
@@ -412,43 +454,29 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1], const Coef<T, REFL>*
 // ------------------------------------------------------------------------------------
 // the persistent pipeline kernel
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, bool STRICT, bool REFL>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
-  using CoefT = Coef<T, REFL>;
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED>
+__device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned char* smem_raw) {
+  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
-  constexpr int CBLK = (K + 1) * K;    // coefficient records per block (wave-major, <= K lanes)
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
   constexpr int S = kStages;
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
   constexpr int NBAR = kCtlWords;
-  constexpr uint32_t kRecBytes = (uint32_t)((K + 1) * sizeof(CoefT));  // one lane's records per block
 
-  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  CoefT* coef_sm = reinterpret_cast<CoefT*>(smem_raw);
-  T* ring_sm = reinterpret_cast<T*>(coef_sm + (size_t)NW * 2 * CBLK);
+  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
-  // "full" is alias-safe as an mbarrier (the consumer has always seen chunk seq-S before it
-  // waits for seq); "consumed" is a monotonic counter because a ring's producer changes
-  // between rounds (previous warp vs. self-fill), which a parity test cannot express.
-  if (threadIdx.x < NW) {
-    uint64_t* bw = bars + threadIdx.x * NBAR;
-#pragma unroll
-    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
-    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
-    mbar_init(bw + S + 1, 1);
-    mbar_init(bw + S + 2, 1);
-  }
-  __syncthreads();
 
   T* const A = reinterpret_cast<T*>(P.A);
   const int len = P.len;
   const int k = P.k;
   const int nchunk = P.nchunk;
   const int nblk = P.nblk;
+  const uint32_t credit = (uint32_t)P.credit;
   uint64_t* const bar_in = bars + warp * NBAR;  // in-ring of this warp: full[S], consumed, coef[2]
   uint64_t* const full_in = bar_in;
   uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
@@ -458,7 +486,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
-  CoefT* const cbuf = coef_sm + (size_t)warp * 2 * CBLK;
+  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
 
   const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
   const long long npos = cr.g1 - cr.g0;
@@ -494,18 +522,26 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
       gcs[r] = ok ? P.cs : 0;
     }
-    // this unit's coefficient blocks: Kb*(K+1) contiguous records per block (rs_pack_kernel)
-    const size_t part_recs = (size_t)k * nblk * (K + 1);
-    const CoefT* const ubase = reinterpret_cast<const CoefT*>(P.coef) + (tile < P.t1 ? part_recs : 0) +
-                               (size_t)p0 * nblk * (K + 1);
-    const uint32_t blk_bytes = (uint32_t)Kb * kRecBytes;
+    // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
+    // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
+    const int part = tile < P.t1 ? 1 : 0;
+    const int brec = Kb * (K + 1) + (SCALED ? kScaleRecs : 0);
+    const CoefT* ubase;
+    if constexpr (SCALED) {
+      const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
+      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
+              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
+    } else {
+      ubase = reinterpret_cast<const CoefT*>(P.coef) + (size_t)part * k * nblk * (K + 1) + (size_t)p0 * nblk * (K + 1);
+    }
+    const uint32_t blk_bytes = (uint32_t)(brec * sizeof(CoefT));
     // one elected lane: WAR fence for the buffer's previous readers, arm, start the copy
     auto issue_coef = [&](int b, uint32_t buf) {
       if (lane == 0) {
         uint64_t* bar = &cbar[buf];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_expect_tx(bar, blk_bytes);
-        bulk_g2s_nowait(cbuf + (size_t)buf * CBLK, ubase + (size_t)b * Kb * (K + 1), blk_bytes, bar);
+        bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
       }
     };
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
@@ -600,10 +636,12 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
       unsigned long long t2 = trace_clock();
       if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
       unsigned long long t3 = trace_clock();
-      if (outring && has_out && oseq >= (uint32_t)S) wait_count(consumed_out, oseq - S + 1u);
+      // ring credit: the producer runs at most `credit` chunks ahead of its consumer
+      if (outring && has_out && oseq >= credit) wait_count(consumed_out, oseq - credit + 1u);
       unsigned long long t4 = trace_clock();
-      run_block<T, K, R, KB, STRICT, REFL, EDGE>(w, cbuf + (cseq & 1) * CBLK, islot, op, ostr, b, len, Kb, lane,
-                                                 b < nchunk, b >= 1);
+      run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED>(
+          w, reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF), islot, op, ostr, b, len, Kb, lane, b < nchunk,
+          b >= 1);
       __syncwarp();
       unsigned long long t5 = trace_clock();
       if (lane == 0) {
@@ -652,6 +690,36 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
     trace_unit(warp, jr, tile, p0, Kb, src, dst, tacc);
   }
+}
+
+template <typename T, int K, int R, bool STRICT, bool REFL>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
+  constexpr int S = kStages;
+  constexpr int NBAR = kCtlWords;
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NW = P.nw;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * CBUF + (size_t)NW * S * (K + 1) * 32 * R * sizeof(T));
+  // "full" is alias-safe as an mbarrier (the consumer has always seen chunk seq-S before it
+  // waits for seq); "consumed" is a monotonic counter because a ring's producer changes
+  // between rounds (previous warp vs. self-fill), which a parity test cannot express.
+  if (threadIdx.x < NW) {
+    uint64_t* bw = bars + threadIdx.x * NBAR;
+#pragma unroll
+    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
+    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
+    mbar_init(bw + S + 1, 1);
+    mbar_init(bw + S + 2, 1);
+  }
+  __syncthreads();
+  // fast fp64: the scaled form, unless the pack found coefficients outside its safe range
+  if constexpr (!STRICT && sizeof(T) == 8) {
+    if (P.use_scaled && *P.unsafe == 0u) {
+      pipeline_units<T, K, R, STRICT, REFL, true>(P, smem_raw);
+      return;
+    }
+  }
+  pipeline_units<T, K, R, STRICT, REFL, false>(P, smem_raw);
 }
 
 // ------------------------------------------------------------------------------------
@@ -703,6 +771,88 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
       }
       dst[((size_t)b * (K + 1) + u) * kb] = cf;
     }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// scaled ("fast Givens") repack for fast-mode fp64. Inside a unit every column j carries a
+// scale sigma_j (1 at unit entry) and the window holds x~ = x / sigma. With (c, s) in
+// forward form, rotation (j, p) is
+//   x' = c*x + s*y = c*sx * (x~ + tau1*y~),  tau1 = s*sy / (c*sx),   sx' = c*sx
+//   y' = c*y - s*x = c*sy * (y~ - tau2*x~),  tau2 = s*sx / (c*sy),   sy' = c*sy
+// (reflector: y' = s*x - c*y, same taus, sy' = -c*sy), i.e. 2 FMAs instead of 2 MUL +
+// 2 FMA. The scales depend only on C/S, so they are computed here, once per call:
+// thread (partition, unit, column j) walks the unit's sweeps in application order
+// (rotation (j-1, p) before (j, p) before (j+1, p)). The column's final scale is applied
+// when the kernel emits it. Records: (tau1, -tau2) at [b][u*kb + l] as in rs_pack_kernel,
+// then the K+1 emission scales of the block. A coefficient that would push a scale or tau
+// outside [2^-256, 2^256] (or c == 0) sets *unsafe and the kernel uses the standard form.
+// ------------------------------------------------------------------------------------
+template <typename T, bool REFL>
+__global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restrict__ out, const T* __restrict__ C,
+                                                             const T* __restrict__ Sm, long long ldcs, int len, int k,
+                                                             int nblk, int ua, int nparts, int rev,
+                                                             uint32_t* __restrict__ unsafe) {
+  constexpr int K = kK;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= len) return;
+  auto coef = [&](int jj, int p, T& c, T& s) {  // forward-form (c, s) of rotation (jj, p)
+    const long long jr = rev ? (long long)(len - 2 - jj) : (long long)jj;
+    c = C[jr + (long long)p * ldcs];
+    s = Sm[jr + (long long)p * ldcs];
+    if (rev) {
+      if constexpr (REFL) {
+        c = -c;
+      } else {
+        s = -s;
+      }
+    }
+  };
+  const T lo = 0x1p-256, hi = 0x1p256;
+  for (int row = blockIdx.y; row < nparts * (ua + 1); row += gridDim.y) {
+    const int part = row / (ua + 1);
+    const int i = row - part * (ua + 1);  // unit index within the tile
+    const int ut = ua + part;
+    if (i >= ut) continue;
+    const int p0 = (int)(((long long)i * k) / ut);
+    const int kb = (int)(((long long)(i + 1) * k) / ut) - p0;
+    const int brec = kb * (K + 1) + kScaleRecs;
+    SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
+                      (size_t)i * nblk * kScaleRecs;
+    T sa = 1, sb = 1;  // running scales of columns j and j+1
+    bool bad = false;
+    for (int l = 0; l < kb; ++l) {
+      const int p = p0 + l;
+      T c, s;
+      if (j >= 1) {  // rotation (j-1, p) touched column j as its y
+        coef(j - 1, p, c, s);
+        sa *= REFL ? -c : c;
+      }
+      if (j <= len - 2) {
+        coef(j, p, c, s);
+        const T t1 = s * sb / (c * sa);
+        const T t2 = s * sa / (c * sb);
+        bad |= !(c != T(0)) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
+        // rotation (j, p) runs in block b at wave u with b(K+1) + u = j + 1 + l
+        const int bu = j + 1 + l;
+        const int b = bu / (K + 1), u = bu - b * (K + 1);
+        SCoef<T> rec{};
+        rec.c = t1;
+        rec.s = -t2;
+        ubase[(size_t)b * brec + u * kb + l] = rec;
+        sa *= c;
+        sb *= REFL ? -c : c;
+        if (j + 1 <= len - 2) {  // rotation (j+1, p) touches column j+1 as its x
+          coef(j + 1, p, c, s);
+          sb *= c;
+        }
+      }
+      bad |= !(fabs(sa) >= lo && fabs(sa) <= hi) || !(fabs(sb) >= lo && fabs(sb) <= hi);
+    }
+    // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
+    const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
+    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)kb * (K + 1))[ue] = sa;
+    if (bad) atomicOr(unsafe, 1u);
   }
 }
 
@@ -767,8 +917,10 @@ struct Geometry {
   int nchunk = 0;
   int nblk = 0;
   size_t coef_rec = 0;
-  size_t coef_bytes = 0;
-  size_t flag_bytes = 0;
+  size_t std_bytes = 0;     // standard records (both sweep partitions)
+  size_t coef_bytes = 0;    // standard + scaled records
+  size_t flags_only = 0;    // progress flags (zeroed per launch)
+  size_t flag_bytes = 0;    // flags + unsafe word + trash slot
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -787,8 +939,11 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
   g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 * tsz : 16);
   // two sweep partitions (ua and ua+1 units per tile) of k * nblk * (K+1) records each
-  g->coef_bytes = align_up(2 * (size_t)g->k * g->nblk * (kK + 1) * g->coef_rec, 256);
-  g->flag_bytes = align_up((size_t)(g->pairs + 1) * sizeof(uint32_t), 256) + kTrashBytes;
+  g->std_bytes = align_up(2 * (size_t)g->k * g->nblk * (kK + 1) * g->coef_rec, 256);
+  // scaled form: per partition k*nblk*(K+1) records + <= k*nblk*kScaleRecs scale records
+  g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (kK + 1 + kScaleRecs) * 16, 256);
+  g->flags_only = align_up((size_t)(g->pairs + 1) * sizeof(uint32_t), 256);
+  g->flag_bytes = g->flags_only + 256 + kTrashBytes;
   return true;
 }
 
@@ -802,8 +957,10 @@ struct LaunchPlan {
 };
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec) {
-  return 2 * (size_t)(kK + 1) * kK * coef_rec + (size_t)kStages * (kK + 1) * kTileOwners * tsz +
-         kCtlWords * sizeof(uint64_t);
+  size_t cbuf = (size_t)(kK + 1) * kK * coef_rec;  // == coef_buf_bytes<T, REFL>()
+  const size_t scl = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
+  if (scl > cbuf) cbuf = scl;
+  return 2 * cbuf + (size_t)kStages * (kK + 1) * kTileOwners * tsz + kCtlWords * sizeof(uint64_t);
 }
 
 // Grid of G <= #SMs persistent CTAs and U = 4*G*q units (q per SM sub-partition, each
@@ -865,7 +1022,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
 
 template <typename T, bool REFL>
 rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs, int rev, void* ws,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool scaled) {
   using CoefT = Coef<T, REFL>;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
   LaunchPlan lp;  // the unit partition of the sweeps comes from the launch plan
@@ -880,6 +1037,19 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   rs_pack_kernel<T, REFL><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk,
                                                                              lp.ua, nparts, rev);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if constexpr (sizeof(T) == 8) {
+    if (scaled) {
+    unsigned char* base = reinterpret_cast<unsigned char*>(ws);
+    uint32_t* unsafe = reinterpret_cast<uint32_t*>(base + g.coef_bytes + g.flags_only);
+    cudaError_t e0 = cudaMemsetAsync(unsafe, 0, sizeof(uint32_t), st);
+    if (e0 != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e0));
+    const int srows = nparts * (lp.ua + 1);
+    const int sy = srows < 65535 ? srows : 65535;
+    rs_pack_scaled_kernel<T, REFL><<<dim3((unsigned)((g.len + 127) / 128), (unsigned)sy), 128, 0, st>>>(
+        reinterpret_cast<SCoef<T>*>(base + g.std_bytes), C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts, rev, unsafe);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
   return RS_OK;
@@ -887,15 +1057,21 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
 
 // Runs the pipeline on coefficients already packed into `ws` (by launch_pack with the
 // same geometry, order and kind). Resets the hand-off flags first.
+bool scaled_disabled() {
+  const char* e = getenv("RS_NO_SCALED");
+  return e != nullptr && atoi(e) != 0;
+}
+
 template <typename T, bool STRICT, bool REFL>
 rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st) {
+  const int use_scaled = (!STRICT && sizeof(T) == 8 && !scaled_disabled()) ? 1 : 0;
   using CoefT = Coef<T, REFL>;
   LaunchPlan lp;
   rs_status rc = plan_launch(g, sizeof(T), &lp);
   if (rc != RS_OK) return rc;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
   uint32_t* flags = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes);
-  cudaError_t e = cudaMemsetAsync(flags, 0, g.flag_bytes - kTrashBytes, st);
+  cudaError_t e = cudaMemsetAsync(flags, 0, g.flags_only, st);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e));
   PipeParams P;
   P.A = Abase;
@@ -909,7 +1085,15 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.ua = lp.ua;
   P.coef = coef;
   P.flags = flags;
-  P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flag_bytes - kTrashBytes;
+  P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only + 256;
+  P.coef_scaled = reinterpret_cast<unsigned char*>(ws) + g.std_bytes;
+  P.unsafe = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only);
+  P.use_scaled = use_scaled;
+  P.credit = kStages;
+  if (const char* ev = getenv("RS_CREDIT")) {
+    const int v = atoi(ev);
+    if (v >= 1 && v <= kStages) P.credit = v;
+  }
   P.len = g.len;
   P.k = g.k;
   P.nchunk = g.nchunk;
@@ -1009,8 +1193,8 @@ rs_status pack_impl(const T* C, const T* S, int64_t ldcs, int64_t m, int64_t n, 
   if (rc != RS_OK) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int rev = order == RS_ORDER_REVERSE;
-  return kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st)
-                                   : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st);
+  return kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, true)
+                                   : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, true);
 }
 
 template <typename T>
@@ -1060,8 +1244,9 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   } else if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) {
     return fail(RS_EINVAL, "workspace must be 256-byte aligned");
   }
-  rs_status rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st)
-                                           : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st);
+  const bool scaled = !strict && !scaled_disabled();
+  rs_status rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, scaled)
+                                           : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, scaled);
   if (rc == RS_OK) rc = run_dispatch<T>(g, A, rev, kind, strict, ws, st);
   if (owned) {
     cudaError_t e = cudaFreeAsync(ws, st);

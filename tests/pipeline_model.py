@@ -1,21 +1,20 @@
-"""CPU model of the CUDA band-pipeline's work split and hand-off protocol.
+"""CPU model of the CUDA pipeline's work split and hand-off protocol.
 
-Mirrors ``rs_pipeline_kernel`` in paper_2412_01852_b200/csrc/rotseq_b200.cu:
-unit list split over CTAs, the in-CTA processing order (tail-first reorder),
-rounds of NW warps, src/dst selection (ring vs. global vs. progress flag),
-ring full/empty barriers with S stages, and per-unit progress flags.
+Mirrors ``plan_launch`` / ``unit_at`` / ``cta_range`` / ``rs_pipeline_kernel`` in
+paper_2412_01852_b200/csrc/rotseq_b200.cu: U units numbered tile-major (tile t holds
+ua (+1 for t < t1) units splitting the k sweeps evenly), G CTAs with contiguous unit
+ranges (the last partial tile first), positions on warp p % NW in rounds, ring
+hand-offs between neighbouring positions of a round, progress flags otherwise.
 
-``simulate`` steps every warp as far as its waits allow (round-robin, one block
-at a time) and reports a deadlock if no warp can make progress. It also records
-the order in which transforms (q, p) are applied to each owner line so the
-schedule's dependency legality can be checked against the reference's rule
-(conftest.py:26-43 ``assert_naive_equivalent_order``).
+``simulate`` steps every warp as far as its waits allow (round-robin, one block at a
+time) and reports a deadlock if no warp can make progress. It also records the order
+of (tile, unit, block) events so the schedule's dependency legality can be checked
+against the reference's rule (conftest.py:26-43 ``assert_naive_equivalent_order``).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass, field
-
+from dataclasses import dataclass
 
 FLAG_EVERY = 8  # kFlagEvery in rotseq_b200.cu
 
@@ -27,23 +26,11 @@ class Geometry:
     k: int
     K: int = 8
     R: int = 2
-    S: int = 3
-
-    @property
-    def tile_owners(self):
-        return 32 * self.R
-
-    @property
-    def bands(self):
-        return -(-self.k // self.K)
+    S: int = 2
 
     @property
     def tiles(self):
-        return -(-self.owners // self.tile_owners)
-
-    @property
-    def units(self):
-        return self.tiles * self.bands
+        return -(-self.owners // (32 * self.R))
 
     @property
     def nchunk(self):
@@ -54,183 +41,152 @@ class Geometry:
         return self.nchunk + 1
 
 
-def warp_cap(dtype_bytes: int = 8, refl: bool = False, R: int = 2, K: int = 8, S: int = 3,
+def warp_cap(dtype_bytes: int = 8, refl: bool = False, R: int = 2, K: int = 8, S: int = 2,
              optin: int = 232448, max_warps: int = 16) -> int:
-    """plan_launch()'s shared-memory bound on warps per CTA."""
+    """plan_launch()'s shared-memory bound on warps per CTA (a multiple of 4)."""
     rec = (4 if refl else 2) * dtype_bytes
-    per = 2 * (K + 1) * K * rec + S * (K + 1) * 32 * R * dtype_bytes + (S + 3) * 8
-    return min(max_warps, (optin - (S + 3) * 8) // per)
+    cbuf = max((K + 1) * K * max(rec, 16), ((K + 1) * K + 5) * 16)
+    per = 2 * cbuf + S * (K + 1) * 32 * R * dtype_bytes + (S + 3) * 8
+    return min(max_warps, (optin - (S + 3) * 8) // per) & ~3
 
 
-def plan(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None):
-    """plan_launch(): grid, warps per CTA."""
-    import math
+def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mode: int = 0):
+    """plan_launch(): grid, U, ua, t1, NW."""
+    cap = max(4, cap & ~3)
+    G = sms if grid is None else min(grid, sms)
+    umin = g.tiles * -(-g.k // g.K)
+    G = max(1, min(G, -(-umin // 4)))
+    q = -(-umin // (4 * G))
+    if mode == 0:
+        mode = 2 if q >= 8 else 1
+    U = 4 * G * q if mode == 1 else umin
+    U = min(U, g.tiles * g.k)
+    nmax = -(-U // G)
+    nw = min(cap, -(-nmax // 4) * 4)
+    return dict(G=G, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw)
 
-    G = min(sms if grid is None else grid, g.units)
-    G = max(G, 1)
-    x = g.units / G
-    rounds = max(1, math.ceil(x / cap))
-    nw = min(cap, max(1, math.ceil(x / rounds)))
-    return G, nw
+
+def tile_first_unit(t, t1, ua):
+    return t * (ua + 1) if t < t1 else t1 * (ua + 1) + (t - t1) * ua
 
 
-def cta_schedule(g: Geometry, G: int, nw: int, c: int):
-    """List of (position, warp, round, unit, src, dst) for CTA c."""
-    U, bands = g.units, g.bands
-    ub, ue = U * c // G, U * (c + 1) // G
-    tail_start = (ue // bands) * bands
-    reorder = (ue % bands != 0) and tail_start > ub
-    ntail = ue - tail_start if reorder else 0
+def unit_at(gidx, t1, ua, k):
+    big = t1 * (ua + 1)
+    if gidx < big:
+        tile, i, ut = gidx // (ua + 1), gidx % (ua + 1), ua + 1
+    else:
+        r = gidx - big
+        tile, i, ut = t1 + r // ua, r % ua, ua
+    p0 = i * k // ut
+    return tile, p0, (i + 1) * k // ut - p0
 
-    def unit_at(p):
-        return (tail_start + p if p < ntail else ub + (p - ntail)) if reorder else ub + p
 
-    def pos_of(u):
-        return ((u - tail_start) if u >= tail_start else (u - ub + ntail)) if reorder else u - ub
+def cta_range(U, c, G, t1, ua, k):
+    g0, g1 = U * c // G, U * (c + 1) // G
+    nl = 0
+    if g1 > g0:
+        tile, p0, kb = unit_at(g1 - 1, t1, ua, k)
+        if p0 + kb < k:
+            f = tile_first_unit(tile, t1, ua)
+            if f > g0:
+                nl = g1 - f
+    return g0, g1, nl
+
+
+def cta_schedule(g: Geometry, pl: dict, c: int):
+    """List of (pos, warp, round, unit gidx, (tile, p0, kb), src, dst) for CTA c."""
+    U, G, t1, ua, NW, k = pl["U"], pl["G"], pl["t1"], pl["ua"], pl["NW"], g.k
+    g0, g1, nl = cta_range(U, c, G, t1, ua, k)
+
+    def pos_to_unit(p):
+        return g1 - nl + p if p < nl else g0 + p - nl
+
+    def unit_to_pos(u):
+        return u - (g1 - nl) if u >= g1 - nl else u - g0 + nl
 
     out = []
-    for p in range(ue - ub):
-        w, jr = p % nw, p // nw
-        u = unit_at(p)
-        band = u % bands
-        if band == 0:
-            src = "global"
-        elif w > 0 and u - 1 >= ub and pos_of(u - 1) == p - 1:
-            src = "ring"
-        else:
-            src = "flag"
-        if band == bands - 1:
-            dst = "global"
-        elif w < nw - 1 and u + 1 < ue and pos_of(u + 1) == p + 1:
-            dst = "ring"
-        else:
-            dst = "flag"
-        out.append((p, w, jr, u, src, dst))
+    for p in range(g1 - g0):
+        w, jr = p % NW, p // NW
+        u = pos_to_unit(p)
+        tile, p0, kb = unit_at(u, t1, ua, k)
+        src = "global"
+        if p0 > 0:
+            src = "ring" if (w > 0 and u - 1 >= g0 and unit_to_pos(u - 1) == p - 1) else "flag"
+        dst = "global"
+        if p0 + kb < k:
+            dst = "ring" if (w < NW - 1 and u + 1 < g1 and unit_to_pos(u + 1) == p + 1) else "flag"
+        out.append((p, w, jr, u, (tile, p0, kb), src, dst))
     return out
 
 
-@dataclass
-class WarpState:
-    cta: int
-    warp: int
-    work: list
-    idx: int = 0          # index into work
-    b: int = -1           # -1: unit prologue pending
-    done: bool = False
-    cseq: int = 0
-
-
-@dataclass
-class Sim:
-    g: Geometry
-    G: int
-    nw: int
-    flags: dict = field(default_factory=dict)
-    full: dict = field(default_factory=dict)    # (cta, ring) -> arrivals
-    empty: dict = field(default_factory=dict)
-    applied: dict = field(default_factory=dict)  # tile -> list of (band, b)
-
-
-def simulate(g: Geometry, sms: int = 148, cap: int = 14, grid: int | None = None, max_steps: int = 10_000_000):
-    G, nw = plan(g, sms, cap, grid)
-    sim = Sim(g, G, nw)
-    S, nchunk, nblk = g.S, g.nchunk, g.nblk
+def simulate(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mode: int = 0,
+             max_steps: int = 20_000_000):
+    pl = plan(g, sms, cap, grid, mode)
+    S, nchunk, nblk, NW = g.S, g.nchunk, g.nblk, pl["NW"]
     warps = []
-    for c in range(G):
-        sched = cta_schedule(g, G, nw, c)
-        for w in range(nw):
-            warps.append(WarpState(c, w, [e for e in sched if e[1] == w]))
-    arrivals_full = {}
-    arrivals_empty = {}
-    flags = {}
-    order = {}  # tile -> list of band-block events
-
-    def fa(key):
-        return arrivals_full.get(key, 0)
-
-    def ea(key):
-        return arrivals_empty.get(key, 0)
-
+    for c in range(pl["G"]):
+        sched = cta_schedule(g, pl, c)
+        for w in range(NW):
+            warps.append(dict(cta=c, warp=w, work=[e for e in sched if e[1] == w], idx=0, b=-1))
+    full, consumed, flags, order = {}, {}, {}, {}
+    active = [ws for ws in warps if ws["work"]]
     steps = 0
-    active = [ws for ws in warps if ws.work]
     while active:
         progressed = False
         for ws in active:
-            if ws.done:
-                continue
-            p, w, jr, u, src, dst = ws.work[ws.idx]
+            p, w, jr, u, (tile, p0, kb), src, dst = ws["work"][ws["idx"]]
             seq0 = jr * nchunk
-            ring_in = (ws.cta, w)
-            ring_out = (ws.cta, w + 1)
-            if ws.b == -1:
-                # prologue: self-fill chunk 0
+            rin, rout = (ws["cta"], w), (ws["cta"], w + 1)
+            myflag, outflag = (tile, p0), (tile, p0 + kb)
+            if ws["b"] == -1:  # prologue: self-fill chunk 0
                 if src != "ring":
-                    if src == "flag" and flags.get(u, 0) < min(2, nchunk):
+                    if src == "flag" and flags.get(myflag, 0) < 1:
                         continue
-                    arrivals_full[ring_in] = fa(ring_in) + 1
-                ws.b = 0
+                    full[rin] = full.get(rin, 0) + 1
+                ws["b"] = 0
                 progressed = True
                 continue
-            b = ws.b
-            self_next = src != "ring" and b + 1 < nchunk
-            self_next2 = src != "ring" and b + 2 < nchunk
-            if self_next2 and src == "flag" and flags.get(u, 0) < b + 3:
+            b = ws["b"]
+            self_fill = src != "ring"
+            if self_fill and b + 1 < nchunk and src == "flag" and flags.get(myflag, 0) < b + 2:
                 continue
             has_in, has_out = b < nchunk, b >= 1
-            iseq = seq0 + b
-            if has_in and fa(ring_in) < iseq + 1:
+            iseq, oseq = seq0 + b, seq0 + b - 1
+            if has_in and full.get(rin, 0) < iseq + 1:
                 continue
-            oseq = seq0 + b - 1
-            if dst == "ring" and has_out and oseq >= S and ea(ring_out) < oseq - S + 1:
+            if dst == "ring" and has_out and oseq >= S and consumed.get(rout, 0) < oseq - S + 1:
                 continue
-            # compute block b
-            tile, band = divmod(u, g.bands)
-            order.setdefault(tile, []).append((band, b))
+            order.setdefault(tile, []).append((p0, kb, b))
             if has_in:
-                arrivals_empty[ring_in] = ea(ring_in) + 1
+                consumed[rin] = iseq + 1
             if dst == "ring" and has_out:
-                arrivals_full[ring_out] = fa(ring_out) + 1
-            if dst == "flag" and has_out and (b % FLAG_EVERY == 0 or b == nblk - 1):
-                flags[u + 1] = b
-            if self_next:
-                arrivals_full[ring_in] = fa(ring_in) + 1
-            ws.b += 1
-            if ws.b >= nblk:
-                ws.idx += 1
-                ws.b = -1
-                if ws.idx >= len(ws.work):
-                    ws.done = True
+                full[rout] = full.get(rout, 0) + 1
+            if dst == "flag" and has_out and (b < 2 * FLAG_EVERY or b % FLAG_EVERY == 0 or b == nblk - 1):
+                flags[outflag] = b
+            if self_fill and b + 1 < nchunk:
+                full[rin] = full.get(rin, 0) + 1
+            ws["b"] += 1
+            if ws["b"] >= nblk:
+                ws["idx"] += 1
+                ws["b"] = -1
             progressed = True
             steps += 1
             if steps > max_steps:
                 raise RuntimeError("step limit exceeded")
-        active = [ws for ws in active if not ws.done]
+        active = [ws for ws in active if ws["idx"] < len(ws["work"])]
         if not progressed:
-            stuck = [(ws.cta, ws.warp, ws.work[ws.idx], ws.b) for ws in active][:12]
-            raise RuntimeError(f"deadlock: G={G} nw={nw}; stuck warps (cta, warp, work, block): {stuck}")
-    return dict(G=G, nw=nw, order=order)
+            stuck = [(ws["cta"], ws["warp"], ws["work"][ws["idx"]], ws["b"]) for ws in active][:12]
+            raise RuntimeError(f"deadlock: {pl}; stuck warps (cta, warp, work, block): {stuck}")
+    return dict(plan=pl, order=order)
 
 
-def check_band_block_order(g: Geometry, order: dict):
-    """Band b+1 block j may only run after band b produced the chunk it reads."""
-    for tile, ev in order.items():
-        done = {}
-        for band, b in ev:
-            done[band] = b
-            if band > 0 and b < g.nchunk:
-                # chunk b of band `band` input = output chunk b of band-1, emitted in its block b+1
-                prev = done.get(band - 1, -1)
-                assert prev >= min(b + 1, g.nblk - 1), (tile, band, b, prev)
-
-
-def block_rotations(g: Geometry, band: int, b: int):
-    """Rotations (j, p) of block b of a band, in the kernel's order (run_block):
+def unit_block_rotations(g: Geometry, p0: int, kb: int, b: int):
+    """Rotations (j, p) of block b of a unit, in the kernel's order (run_block):
     wave u = 0..K (t = b(K+1)+u-1), lanes l ascending, j = t - l."""
     K = g.K
-    kb = min(K, g.k - band * K)
     for u in range(K + 1):
         t = b * (K + 1) + u - 1
         for lane in range(kb):
             j = t - lane
             if 0 <= j <= g.length - 2:
-                yield j, band * K + lane
+                yield j, p0 + lane

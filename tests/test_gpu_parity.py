@@ -122,6 +122,43 @@ def test_fast_mode_tolerances(cuda, oracle_mod, kind):
         assert compare(ref, got, "baseline", k=k).passed
 
 
+@pytest.mark.parametrize("side,order", SIDES_ORDERS)
+@pytest.mark.parametrize("kind", ("rotation", "reflector"))
+def test_fast_mode_scaled_and_standard_forms(cuda, oracle_mod, monkeypatch, side, order, kind):
+    """fp64 fast mode runs the scaled ("fast Givens") records; RS_NO_SCALED=1 forces the
+    standard 2 MUL + 2 FMA form. Both within 10*k*eps of the strict oracle."""
+    from paper_2412_01852_b200 import compare, generate_sequence, make_inputs
+
+    for (m, n, k) in ((70, 90, 17), (130, 600, 40)):
+        A0, seq = make_inputs(m, n, k, 2)
+        if side == "left":
+            seq = generate_sequence(m, k, 5)
+        ref = A0.copy(order="F")
+        oracle_mod.apply_naive(ref, seq.C, seq.S, side=side, order=order, kind=kind)
+        for flag in ("0", "1"):
+            monkeypatch.setenv("RS_NO_SCALED", flag)
+            got = _gpu(A0, seq.C, seq.S, side=side, order=order, kind=kind, fast=True)
+            rep = compare(ref, got, "baseline", k=k)
+            assert rep.passed, f"RS_NO_SCALED={flag} {m}x{n} k={k} {side} {order} {kind}: {rep}"
+
+
+@pytest.mark.parametrize("kind", ("rotation", "reflector"))
+def test_fast_mode_unsafe_coefficients_fall_back(cuda, oracle_mod, kind):
+    """Quarter turns (c == 0) have no scaled form: the pack flags them and the kernel
+    runs the standard records, still within tolerance (and exact for c=0, s=1 swaps)."""
+    from paper_2412_01852_b200 import compare, make_inputs
+
+    m, n, k = 200, 300, 24
+    A0, seq = make_inputs(m, n, k, 4)
+    C, S = seq.C.copy(), seq.S.copy()
+    C[::7, ::3], S[::7, ::3] = 0.0, 1.0
+    ref = A0.copy(order="F")
+    oracle_mod.apply_naive(ref, C, S, kind=kind)
+    got = _gpu(A0, C, S, kind=kind, fast=True)
+    rep = compare(ref, got, "baseline", k=k)
+    assert rep.passed and np.isfinite(got).all(), rep
+
+
 def test_fp32_strict_bitwise_vs_numpy_fp32_oracle(cuda, oracle_mod):
     for (m, n, k, side, order) in ((65, 33, 12, "right", "forward"), (100, 70, 17, "left", "reverse"),
                                    (31, 200, 40, "right", "reverse")):

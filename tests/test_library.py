@@ -44,12 +44,14 @@ def test_version_and_workspace_formula():
     lib = _lib.load()
     assert lib.rs_version() >= 10300
     ws = lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 0)
-    # two sweep partitions x 192 sweeps x 457 blocks x 9 waves of 16 B records,
-    # + 64 tiles x 192 progress flags + trash slot
+    # two sweep partitions x 192 sweeps x 457 blocks x 9 waves of 16 B records
+    # (standard form) + the same with 5 scale records per block (scaled form),
+    # + 64 tiles x 192 progress flags + unsafe word + trash slot
     nblk = (4096 + 8) // 9 + 1
     coef = -(-2 * 192 * nblk * 9 * 16 // 256) * 256
+    scaled = -(-2 * 192 * nblk * 14 * 16 // 256) * 256
     flags = -(-(64 * 192 + 1) * 4 // 256) * 256
-    assert ws == coef + flags + 32 * 2 * 8
+    assert ws == coef + scaled + flags + 256 + 32 * 2 * 8
     assert ws % 256 == 0
     assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 1, 0) > ws  # reflector records are 32 B
     assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 1) == ws  # fp32 records padded to 16 B

@@ -6,7 +6,8 @@
   dependency-legal order (the reference's assert_naive_equivalent_order,
   conftest.py:26-43);
 * a numpy emulation of the register-window slots and the packed coefficient records
-  reproduces the oracle bit for bit (kernel_emulator).
+  reproduces the oracle bit for bit (kernel_emulator), and the fast-mode scaled records
+  reproduce it within the fast-mode tolerance.
 """
 
 from __future__ import annotations
@@ -15,8 +16,8 @@ import numpy as np
 import pytest
 
 from conftest import assert_bitwise, assert_naive_equivalent_order
-from kernel_emulator import emulate
-from pipeline_model import Geometry, block_rotations, simulate, warp_cap
+from kernel_emulator import emulate, pack_unit_scaled, unit_partition
+from pipeline_model import Geometry, plan, simulate, unit_block_rotations, warp_cap
 
 
 @pytest.mark.parametrize("owners,length,k,dtype_bytes,refl", [
@@ -30,35 +31,58 @@ from pipeline_model import Geometry, block_rotations, simulate, warp_cap
 def test_protocol_deadlock_free_on_baseline_geometries(owners, length, k, dtype_bytes, refl):
     g = Geometry(owners=owners, length=length, k=k)
     res = simulate(g, cap=warp_cap(dtype_bytes, refl))
-    assert res["G"] >= 1
+    assert res["plan"]["G"] >= 1
 
 
-@pytest.mark.parametrize("cap,grid", [(1, 1), (2, 3), (3, 2), (4, 5), (5, 7), (2, None), (14, 148)])
+@pytest.mark.parametrize("cap,grid", [(4, 1), (4, 3), (8, 2), (4, 5), (8, 7), (4, None), (16, 148)])
 @pytest.mark.parametrize("owners,length,k", [(100, 50, 40), (300, 37, 33), (64, 200, 70), (33, 9, 24),
                                              (700, 20, 100), (129, 300, 8)])
-def test_protocol_deadlock_free_forced_geometries(cap, grid, owners, length, k):
-    """The RS_DEBUG_MAX_WARPS / RS_DEBUG_GRID geometries exercised on the GPU."""
-    simulate(Geometry(owners=owners, length=length, k=k), cap=cap, grid=grid)
+@pytest.mark.parametrize("mode", (1, 2))
+def test_protocol_deadlock_free_forced_geometries(cap, grid, owners, length, k, mode):
+    """The RS_DEBUG_MAX_WARPS / RS_DEBUG_GRID / RS_PLAN_MODE geometries run on the GPU."""
+    simulate(Geometry(owners=owners, length=length, k=k), cap=cap, grid=grid, mode=mode)
 
 
-@pytest.mark.parametrize("length,k", [(2, 1), (3, 5), (9, 8), (10, 8), (17, 9), (40, 24), (33, 100), (64, 7)])
-def test_block_decomposition_is_dependency_legal(length, k):
+def test_plan_balances_sub_partitions():
+    """Config 2: every SM sub-partition gets exactly q units of nearly equal width."""
+    g = Geometry(owners=4096, length=4096, k=192)
+    pl = plan(g, cap=16)
+    assert pl["U"] % (4 * pl["G"]) == 0
+    from pipeline_model import cta_schedule
+    for c in (0, 1, 77, pl["G"] - 1):
+        loads = [0, 0, 0, 0]
+        for _, w, _, _, (_, _, kb), _, _ in cta_schedule(g, pl, c):
+            loads[w % 4] += kb
+        assert max(loads) - min(loads) <= 2, loads
+
+
+@pytest.mark.parametrize("k,ut", [(192, 27), (192, 28), (7, 7), (100, 13), (8, 1)])
+def test_unit_partition_covers_sweeps(k, ut):
+    parts = unit_partition(k, ut)
+    assert parts[0][0] == 0 and sum(kb for _, kb in parts) == k
+    assert all(1 <= kb <= 8 for _, kb in parts) or ut * 8 < k
+    assert all(parts[i][0] + parts[i][1] == parts[i + 1][0] for i in range(ut - 1))
+
+
+@pytest.mark.parametrize("length,k,ut", [(2, 1, 1), (3, 5, 1), (9, 8, 1), (10, 8, 2), (17, 9, 2), (40, 24, 4),
+                                         (33, 100, 13), (64, 7, 3)])
+def test_block_decomposition_is_dependency_legal(length, k, ut):
     g = Geometry(owners=64, length=length, k=k)
     order = []
-    # bands run in pipeline order; any interleaving that respects the ring protocol
-    # keeps band b+1 behind band b per column, so the band-sequential order suffices
-    for band in range(g.bands):
+    # units run in pipeline order; any interleaving that respects the ring protocol
+    # keeps unit i+1 behind unit i per column, so the unit-sequential order suffices
+    for p0, kb in unit_partition(k, ut):
         for b in range(g.nblk):
-            order.extend(block_rotations(g, band, b))
+            order.extend(unit_block_rotations(g, p0, kb, b))
     assert_naive_equivalent_order(order, length, k)
 
 
 def test_pipelined_interleaving_is_dependency_legal():
-    """The actual interleaving of band blocks produced by the protocol model."""
+    """The actual interleaving of unit blocks produced by the protocol model."""
     g = Geometry(owners=200, length=60, k=40)
-    res = simulate(g, cap=3, grid=4)
+    res = simulate(g, cap=4, grid=4)
     for tile, events in res["order"].items():
-        order = [r for band, b in events for r in block_rotations(g, band, b)]
+        order = [r for p0, kb, b in events for r in unit_block_rotations(g, p0, kb, b)]
         assert_naive_equivalent_order(order, g.length, g.k)
 
 
@@ -68,7 +92,7 @@ def test_pipelined_interleaving_is_dependency_legal():
 def test_kernel_emulator_matches_oracle(oracle_mod, side, order, kind):
     from paper_2412_01852_b200 import generate_sequence, make_inputs
 
-    for (m, n, k) in ((7, 12, 3), (5, 20, 11), (9, 3, 9), (4, 2, 1)):
+    for (m, n, k, ut) in ((7, 12, 3, 1), (5, 20, 11, 2), (9, 3, 9, 3), (4, 2, 1, 1), (6, 15, 17, 4)):
         A0, seq = make_inputs(m, n, k, 5)
         C, S = seq.C, seq.S
         if side == "left":
@@ -76,7 +100,38 @@ def test_kernel_emulator_matches_oracle(oracle_mod, side, order, kind):
             C, S = s2.C, s2.S
         ref = A0.copy(order="F")
         oracle_mod.apply_naive(ref, C, S, side=side, order=order, kind=kind)
-        assert_bitwise(ref, emulate(A0, C, S, side, order, kind), f"{m}x{n} k={k} {side} {order} {kind}")
+        assert_bitwise(ref, emulate(A0, C, S, side, order, kind, ut=ut), f"{m}x{n} k={k} {side} {order} {kind}")
+
+
+@pytest.mark.parametrize("side", ("right", "left"))
+@pytest.mark.parametrize("order", ("forward", "reverse"))
+@pytest.mark.parametrize("kind", ("rotation", "reflector"))
+def test_scaled_form_matches_oracle(oracle_mod, side, order, kind):
+    """The fast-mode scaled ("fast Givens") records reproduce the transform within the
+    fast-mode tolerance (relative Frobenius <= 10*k*eps)."""
+    from paper_2412_01852_b200 import compare, generate_sequence, make_inputs
+
+    for (m, n, k, ut) in ((7, 12, 3, 1), (5, 20, 11, 2), (6, 40, 24, 4), (4, 2, 1, 1)):
+        A0, seq = make_inputs(m, n, k, 3)
+        C, S = seq.C, seq.S
+        if side == "left":
+            s2 = generate_sequence(m, k, 4)
+            C, S = s2.C, s2.S
+        ref = A0.copy(order="F")
+        oracle_mod.apply_naive(ref, C, S, side=side, order=order, kind=kind)
+        got = emulate(A0, C, S, side, order, kind, ut=ut, scaled=True)
+        rep = compare(ref, got, "fast", k=k)
+        assert rep.passed, f"{m}x{n} k={k} {side} {order} {kind}: {rep}"
+
+
+def test_scaled_pack_flags_unsafe_coefficients():
+    """c == 0 (a quarter turn) has no scaled form: the pack must report it so the
+    kernel falls back to the standard records."""
+    C = np.full((5, 3), 0.6)
+    S = np.full((5, 3), 0.8)
+    assert not pack_unit_scaled(C, S, 6, 0, 3)[2]
+    C[2, 1], S[2, 1] = 0.0, 1.0
+    assert pack_unit_scaled(C, S, 6, 0, 3)[2]
 
 
 def test_kernel_emulator_golden(golden):
