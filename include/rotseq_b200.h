@@ -116,6 +116,21 @@ rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int6
 rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,
                               int kind, int strict, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Host-buffer entry point: A (m x n, column-major, lda), C and S ((len-1) x k, ldcs) in
+ * HOST memory (pinned for full bandwidth; pageable works, slower). Synchronous: returns
+ * once A holds the result. This is the call a host-side binding of the reference makes
+ * in place of rotseq.core.apply_naive / rotseq.blocking.apply_blocked
+ * (core.py:365-374, blocking.py:420-476) when its data lives in host memory: C/S are
+ * copied and packed, then A streams in and out in wave-column chunks that overlap with
+ * the pipeline kernel (copy-in, compute and copy-out run concurrently). Device buffers
+ * come from the stream-ordered allocator; `stream` orders the compute. */
+rs_status rs_apply_host_f64(double* A, int64_t m, int64_t n, int64_t lda,
+                            const double* C, const double* S, int64_t ldcs, int64_t k,
+                            int side, int order, int kind, int strict, void* stream);
+rs_status rs_apply_host_f32(float* A, int64_t m, int64_t n, int64_t lda,
+                            const float* C, const float* S, int64_t ldcs, int64_t k,
+                            int side, int order, int kind, int strict, void* stream);
+
 /* Launch geometry the pipeline would use for this problem on the current device
  * (for benchmarks / roofline accounting). Any out-pointer may be NULL. */
 rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype,

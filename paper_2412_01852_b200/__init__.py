@@ -32,6 +32,7 @@ from .apply import (  # noqa: F401
     apply_blocked,
     apply_cuda,
     apply_device,
+    apply_host,
     apply_naive,
     workspace_bytes,
 )

@@ -43,6 +43,8 @@ EXPORTS = (
     "rs_pack_f32",
     "rs_apply_packed_f64",
     "rs_apply_packed_f32",
+    "rs_apply_host_f64",
+    "rs_apply_host_f32",
     "rs_launch_count",
     "rs_debug_set_trace",
     "rs_fma_peak_tflops",
@@ -81,6 +83,10 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [vp, i64, i64, i64, i64, i32, i32, i32, i32, vp, sz, vp]
+    for name in ("rs_apply_host_f64", "rs_apply_host_f32"):
+        fn = getattr(lib, name)
+        fn.restype = i32
+        fn.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i32, i32, i32, i32, vp]
     lib.rs_plan_info.restype = i32
     lib.rs_plan_info.argtypes = [i64, i64, i64, i32, i32, i32,
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i64),

@@ -167,6 +167,86 @@ def apply_device(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=S
     _lib.check(st, "rs_apply")
 
 
+def _host_cs(seq, np_dtype, length):
+    """(C, S) as host column-major arrays of the working dtype (copies only if needed)."""
+    if isinstance(seq, RotationSequence):
+        C, S = seq.C, seq.S
+    else:
+        C, S = seq
+    out = []
+    for X, name in ((C, "C"), (S, "S")):
+        if _is_tensor(X):
+            if X.is_cuda:
+                raise ValueError(f"{name} is a CUDA tensor but A is in host memory")
+            X = X.numpy()
+        X = np.asarray(X)
+        if X.ndim != 2:
+            raise ValueError(f"{name} must be 2-D")
+        out.append(np.asfortranarray(X, dtype=np_dtype))
+    if out[0].shape != out[1].shape:
+        raise ValueError(f"C and S must share a 2-D shape, got {out[0].shape} vs {out[1].shape}")
+    if out[0].shape[0] != length - 1:
+        raise ValueError(f"C/S have {out[0].shape[0]} rows, expected {length - 1}")
+    return out[0], out[1]
+
+
+def apply_host(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Side.RIGHT,
+               order=Order.FORWARD, device=None) -> None:
+    """In-place apply on a host matrix (numpy array or CPU torch tensor, column-major)
+    through ``rs_apply_host_*``: C/S are copied and packed, then A streams to the GPU
+    and back in wave-column chunks overlapped with the kernel. Synchronous. Pinned
+    memory (``torch.empty(..., pin_memory=True)``) gives full copy bandwidth."""
+    torch = _torch()
+    kind = _as_enum(kind, TransformKind, "kind")
+    side = _as_enum(side, Side, "side")
+    order = _as_enum(order, Order, "order")
+    if _is_tensor(A):
+        if A.is_cuda:
+            raise ValueError("apply_host needs a host matrix; use apply_device for CUDA tensors")
+        if A.dim() != 2 or A.dtype not in (torch.float64, torch.float32):
+            raise ValueError("A must be a 2-D float64/float32 tensor")
+        if A.shape[0] > 1 and A.stride(0) != 1:
+            raise ValueError("A must be column-major (first stride 1)")
+        m, n = int(A.shape[0]), int(A.shape[1])
+        lda = int(A.stride(1)) if n > 1 else max(m, 1)
+        np_dtype = np.float64 if A.dtype == torch.float64 else np.float32
+        ptr = A.data_ptr()
+    else:
+        if isinstance(seq, RotationSequence):
+            check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
+        else:
+            require_colmajor(A, dtypes=(np.float64, np.float32))
+        m, n = A.shape
+        lda = A.strides[1] // A.itemsize if n > 1 else max(m, 1)
+        np_dtype = A.dtype.type
+        ptr = A.ctypes.data
+    length = m if side is Side.LEFT else n
+    if length < 2:
+        if side is Side.LEFT:
+            raise ValueError(f"matrix needs at least 2 rows for left-side application, got {m}")
+        raise ValueError(f"matrix needs at least 2 columns, got {n}")
+    ncols = _seq_ncols(seq)
+    if ncols != length:
+        what = "rows" if side is Side.LEFT else "columns"
+        raise ValueError(f"sequence acts on {ncols} {what} but matrix has {length}")
+    if m == 0 or n == 0:
+        return
+    C, S = _host_cs(seq, np_dtype, length)
+    k = C.shape[1]
+    lib = _lib.load()
+    f64 = np_dtype == np.float64
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        fn = lib.rs_apply_host_f64 if f64 else lib.rs_apply_host_f32
+        st = fn(ptr, m, n, lda, C.ctypes.data, S.ctypes.data, max(C.shape[0], 1), k,
+                _lib.SIDE_LEFT if side is Side.LEFT else _lib.SIDE_RIGHT,
+                _lib.ORDER_REVERSE if order is Order.REVERSE else _lib.ORDER_FORWARD,
+                _lib.KIND_REFLECTOR if kind is TransformKind.REFLECTOR else _lib.KIND_ROTATION,
+                0 if fast else 1, stream.cuda_stream)
+    _lib.check(st, "rs_apply_host")
+
+
 def workspace_bytes(m: int, n: int, k: int, side=Side.RIGHT, kind=TransformKind.ROTATION,
                     dtype=np.float64) -> int:
     side = _as_enum(side, Side, "side")
@@ -189,6 +269,10 @@ def apply_cuda(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Sid
     torch = _torch()
     if _is_tensor(A) and A.is_cuda:
         apply_device(A, seq, kind, fast, side, order, algo, workspace)
+        return
+    if algo == "pipeline":
+        # host matrix: the streaming host-buffer C-ABI (copies overlap the kernel)
+        apply_host(A, seq, kind, fast, side, order, device)
         return
     if _is_tensor(A):
         # host torch tensor (ideally pinned): async H2D, apply, async D2H, synchronise

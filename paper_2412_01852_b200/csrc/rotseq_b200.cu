@@ -34,6 +34,7 @@
 //     shape (no contraction => bit-identical to the reference strict build); fast mode uses
 //     2 DMUL + 2 DFMA per rotation element (the 4-instruction minimum for 6 flops).
 
+#include <cuda.h>  // stream memory-op types (entry points resolved at run time)
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -314,6 +315,13 @@ struct PipeParams {
   int nw;            // warps per CTA (multiple of 4)
   int use_scaled;    // fast fp64: scaled records were packed
   int credit;        // ring credit in chunks (1..S)
+  // host-streaming mode (rs_apply_host_*): A arrives from the host in wave-column chunks
+  // of cw columns while the kernel runs, and leaves in the same chunks as soon as every
+  // tile's final unit has emitted them. Null pointers: A is resident.
+  const uint32_t* arrived;  // number of chunks already copied in (written by the copy stream)
+  uint32_t* done;           // per chunk: tiles whose final unit has emitted it
+  int cw;                   // chunk width in wave columns
+  int ncw;                  // number of chunks
 };
 
 // ------------------------------------------------------------------------------------
@@ -557,6 +565,12 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     uint32_t flag_seen = 0;
     auto fill_chunk = [&](int q) {
       if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
+      if (src == SRC_GLOBAL && P.arrived != nullptr) {  // host streaming: wait for the copy
+        long long cend = (long long)q * (K + 1) + K;
+        if (cend > len - 1) cend = len - 1;
+        const uint32_t need = (uint32_t)(cend / P.cw) + 1u;
+        if (flag_seen < need) flag_seen = wait_flag(P.arrived, need);
+      }
       T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
       const long long c0 = (long long)q * (K + 1);
       const T* sp[R];
@@ -606,6 +620,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       for (int s = 0; s <= K; ++s) w[r][s] = T(0);
 
     const bool outring = dst == DST_RING;
+    int done_sig = 0;  // host streaming: chunks already released by this (final) unit
     // One block: protocol + compute. KB / EDGE are compile-time so the interior loop
     // carries no per-block branches beyond this unit's hand-off protocol.
     auto block = [&](int b, auto kb_c, auto edge_c) {
@@ -652,6 +667,15 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
           // fence; the release store then publishes "chunks 0..b-1 are in A"
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release(outflag, (uint32_t)b);
+        }
+        if (dst == DST_GLOBAL && has_out && P.done != nullptr) {  // host streaming: release chunks
+          long long e = (long long)b * (K + 1) - 1;  // last column emitted by this block
+          if (e > len - 1) e = len - 1;
+          const int nd = e == len - 1 ? P.ncw : (int)((e + 1) / P.cw);
+          if (nd > done_sig) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (; done_sig < nd; ++done_sig) atomicAdd(P.done + done_sig, 1u);
+          }
         }
       }
       if (self && b + 1 < nchunk) {  // the chunk read by the next block has landed
@@ -1020,6 +1044,13 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   return RS_OK;
 }
 
+struct HostStream {
+  const uint32_t* arrived = nullptr;
+  uint32_t* done = nullptr;
+  int cw = 1;
+  int ncw = 0;
+};
+
 template <typename T, bool REFL>
 rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs, int rev, void* ws,
                       cudaStream_t st, bool scaled) {
@@ -1063,7 +1094,8 @@ bool scaled_disabled() {
 }
 
 template <typename T, bool STRICT, bool REFL>
-rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st) {
+rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st,
+                     const HostStream* hs = nullptr) {
   const int use_scaled = (!STRICT && sizeof(T) == 8 && !scaled_disabled()) ? 1 : 0;
   using CoefT = Coef<T, REFL>;
   LaunchPlan lp;
@@ -1089,6 +1121,10 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.coef_scaled = reinterpret_cast<unsigned char*>(ws) + g.std_bytes;
   P.unsafe = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only);
   P.use_scaled = use_scaled;
+  P.arrived = hs ? hs->arrived : nullptr;
+  P.done = hs ? hs->done : nullptr;
+  P.cw = hs ? hs->cw : 1;
+  P.ncw = hs ? hs->ncw : 0;
   P.credit = kStages;
   if (const char* ev = getenv("RS_CREDIT")) {
     const int v = atoi(ev);
@@ -1142,12 +1178,13 @@ rs_status launch_naive(const Geometry& g, T* A, const T* C, const T* S, long lon
 }
 
 template <typename T>
-rs_status run_dispatch(const Geometry& g, T* A, int rev, int kind, int strict, void* ws, cudaStream_t st) {
+rs_status run_dispatch(const Geometry& g, T* A, int rev, int kind, int strict, void* ws, cudaStream_t st,
+                       const HostStream* hs = nullptr) {
   if (strict)
-    return kind == RS_KIND_REFLECTOR ? launch_run<T, true, true>(g, A, rev, ws, st)
-                                     : launch_run<T, true, false>(g, A, rev, ws, st);
-  return kind == RS_KIND_REFLECTOR ? launch_run<T, false, true>(g, A, rev, ws, st)
-                                   : launch_run<T, false, false>(g, A, rev, ws, st);
+    return kind == RS_KIND_REFLECTOR ? launch_run<T, true, true>(g, A, rev, ws, st, hs)
+                                     : launch_run<T, true, false>(g, A, rev, ws, st, hs);
+  return kind == RS_KIND_REFLECTOR ? launch_run<T, false, true>(g, A, rev, ws, st, hs)
+                                   : launch_run<T, false, false>(g, A, rev, ws, st, hs);
 }
 
 // Shared argument validation (reference: require_colmajor core.py:41-51, _check_apply_args
@@ -1253,6 +1290,234 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
     if (rc == RS_OK && e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFreeAsync: ") + cudaGetErrorString(e));
   }
   return rc;
+}
+
+// ------------------------------------------------------------------------------------
+// host-buffer entry point: A, C, S in host memory (pinned for full PCIe/C2C speed).
+// C/S go first and are packed; A then streams in wave-column chunks on one copy stream
+// while the pipeline kernel runs (its sweep-0 units wait for each chunk's arrival
+// counter, written by a stream memory op after the copy), and every chunk streams back
+// on a second copy stream as soon as all tiles' final units have released it (device
+// counter awaited by a stream wait-value op). Copy-in, compute and copy-out overlap.
+// ------------------------------------------------------------------------------------
+typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+struct StreamOps {
+  PFN_writeValue32 write = nullptr;
+  PFN_waitValue32 wait = nullptr;
+  bool ok = false;
+};
+
+const StreamOps& stream_ops() {
+  static StreamOps ops = [] {
+    StreamOps o;
+    void* fw = nullptr;
+    void* fv = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    // the v2 stream memory ops (CUDA >= 12.0 ABI) are always available
+    if (cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &fw, 12000, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &fv, 12000, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+      o.write = reinterpret_cast<PFN_writeValue32>(fw);
+      o.wait = reinterpret_cast<PFN_waitValue32>(fv);
+      o.ok = true;
+    }
+    return o;
+  }();
+  return ops;
+}
+
+// 2-D copy that degrades to a linear copy when both pitches equal the width (the copy
+// engines run linear copies at full link speed; strided ones are slower)
+cudaError_t copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                   cudaMemcpyKind kind, cudaStream_t st) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * height, kind, st);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, st);
+}
+
+// copy wave columns [v0, v1) of A between host (lda) and device (dense, ld = m)
+template <typename T>
+cudaError_t copy_wave_chunk(T* dev, T* host, const Geometry& g, int64_t m, int64_t lda, int rev, long long v0,
+                            long long v1, cudaMemcpyKind kind, cudaStream_t st) {
+  const long long p0 = rev ? g.len - v1 : v0;  // physical first column (right) / row (left)
+  const long long cnt = v1 - v0;
+  const bool left = g.os != 1;  // owners are columns
+  T* dptr;
+  T* hptr;
+  size_t width, height;
+  if (!left) {
+    dptr = dev + p0 * m;
+    hptr = host + p0 * lda;
+    width = (size_t)m * sizeof(T);
+    height = (size_t)cnt;
+  } else {
+    dptr = dev + p0;
+    hptr = host + p0;
+    width = (size_t)cnt * sizeof(T);
+    height = (size_t)g.owners;
+  }
+  if (kind == cudaMemcpyHostToDevice)
+    return copy2d(dptr, (size_t)m * sizeof(T), hptr, (size_t)lda * sizeof(T), width, height, kind, st);
+  return copy2d(hptr, (size_t)lda * sizeof(T), dptr, (size_t)m * sizeof(T), width, height, kind, st);
+}
+
+struct HostCtx {
+  int dev = -1;
+  cudaStream_t cin = nullptr, cout = nullptr;
+  cudaEvent_t e0 = nullptr, ecs = nullptr, eend = nullptr;
+  uint32_t* ctl = nullptr;  // arrival / release counters (cudaMalloc: stream memory ops
+                            // reject stream-ordered pool addresses)
+};
+constexpr int kMaxHostChunks = 64;
+
+template <typename T>
+rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs, int64_t k,
+                          int side, int order, int kind, int strict, void* stream) {
+  const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
+  Geometry gh;
+  rs_status rc = validate(m, n, lda, ldcs, k, side, order, kind, dtype, true, &gh);
+  if (rc != RS_OK) return rc;
+  if (gh.owners == 0) return RS_OK;
+  if (!A || !C || !S) return fail(RS_EINVAL, "null pointer");
+  const StreamOps& ops = stream_ops();
+  if (!ops.ok) return fail(RS_EUNSUPPORTED, "stream memory operations unavailable");
+  Geometry g;  // device copy of A is dense: ld = m
+  make_geometry(m, n, m > 1 ? m : 1, k, side, kind, dtype, &g);
+  const int rev = order == RS_ORDER_REVERSE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static thread_local HostCtx ctx;
+  if (ctx.dev != dev) {
+    if (cudaStreamCreateWithFlags(&ctx.cin, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx.cout, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx.e0, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx.ecs, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx.eend, cudaEventDisableTiming) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void**>(&ctx.ctl), (kMaxHostChunks + 1) * sizeof(uint32_t)) != cudaSuccess)
+      return fail(RS_ECUDA, "stream/event/counter creation failed");
+    ctx.dev = dev;
+    // keep stream-ordered allocations cached between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  // wave-column chunks: ~32 per call, at least 64 columns each
+  int nchunks_target = 8;
+  if (const char* ev = getenv("RS_HOST_CHUNKS")) {
+    const int v = atoi(ev);
+    if (v >= 1 && v <= kMaxHostChunks) nchunks_target = v;
+  }
+  int cw = (int)((g.len + nchunks_target - 1) / nchunks_target);
+  if (cw < 64) cw = 64;
+  const int ncw = (int)((g.len + cw - 1) / cw);
+  const size_t abytes = (size_t)m * n * sizeof(T);
+  const size_t csbytes = (size_t)(g.len - 1) * k * sizeof(T);
+  const size_t wsbytes = g.coef_bytes + g.flag_bytes;
+  const size_t ctlbytes = (size_t)(ncw + 1) * sizeof(uint32_t);
+  unsigned char* mem = nullptr;
+  const size_t off_c = align_up(abytes, 256), off_s = off_c + align_up(csbytes, 256);
+  const size_t off_ws = off_s + align_up(csbytes, 256), off_ctl = off_ws + align_up(wsbytes, 256);  // = total
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&mem), off_ctl, st);
+  if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("device buffers: ") + cudaGetErrorString(e));
+  T* dA = reinterpret_cast<T*>(mem);
+  T* dC = reinterpret_cast<T*>(mem + off_c);
+  T* dS = reinterpret_cast<T*>(mem + off_s);
+  void* ws = mem + off_ws;
+  uint32_t* ctl = ctx.ctl;  // [0] arrived, [1..ncw] done
+  HostStream hs;
+  hs.arrived = ctl;
+  hs.done = ctl + 1;
+  hs.cw = cw;
+  hs.ncw = ncw;
+  auto ck = [&](cudaError_t x, const char* what) -> bool {
+    if (x != cudaSuccess && e == cudaSuccess) {
+      e = x;
+      g_err = std::string(what) + ": " + cudaGetErrorString(x);
+    }
+    return x == cudaSuccess;
+  };
+  e = cudaSuccess;
+  // developer timeline (RS_HOST_DEBUG=1): events on every stream, printed to stderr
+  const bool dbg = getenv("RS_HOST_DEBUG") != nullptr;
+  cudaEvent_t dev_ev[3 * kMaxHostChunks + 8];
+  int nev = 0;
+  const char* ev_name[3 * kMaxHostChunks + 8];
+  auto mark = [&](cudaStream_t s, const char* name) {
+    if (!dbg || nev >= 3 * kMaxHostChunks + 8) return;
+    cudaEventCreate(&dev_ev[nev]);
+    cudaEventRecord(dev_ev[nev], s);
+    ev_name[nev++] = name;
+  };
+  mark(st, "start");
+  ck(cudaMemsetAsync(ctl, 0, ctlbytes, st), "memset");
+  ck(cudaEventRecord(ctx.e0, st), "event");
+  // copy-in stream: C, S, then A chunk by chunk, each followed by its arrival count
+  ck(cudaStreamWaitEvent(ctx.cin, ctx.e0, 0), "wait");
+  const size_t lc = (size_t)(g.len - 1);
+  ck(copy2d(dC, lc * sizeof(T), C, (size_t)ldcs * sizeof(T), lc * sizeof(T), (size_t)k, cudaMemcpyHostToDevice,
+            ctx.cin), "C copy");
+  ck(copy2d(dS, lc * sizeof(T), S, (size_t)ldcs * sizeof(T), lc * sizeof(T), (size_t)k, cudaMemcpyHostToDevice,
+            ctx.cin), "S copy");
+  ck(cudaEventRecord(ctx.ecs, ctx.cin), "event");
+  mark(ctx.cin, "cs_in");
+  for (int i = 0; i < ncw && e == cudaSuccess; ++i) {
+    if (i == ncw - 1) mark(ctx.cin, "a_in_last_start");
+    const long long v0 = (long long)i * cw, v1 = v0 + cw < g.len ? v0 + cw : g.len;
+    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyHostToDevice, ctx.cin), "A copy-in");
+    const CUresult r = ops.write(reinterpret_cast<CUstream>(ctx.cin), reinterpret_cast<CUdeviceptr>(ctl),
+                                 (cuuint32_t)(i + 1), 0);
+    if (r != CUDA_SUCCESS) {
+      ck(cudaErrorUnknown, "cuStreamWriteValue32");
+      g_err += " (CUresult " + std::to_string((int)r) + ")";
+    }
+  }
+  mark(ctx.cin, "a_in_done");
+  // compute stream: pack once C/S are in, then the streaming pipeline kernel
+  ck(cudaStreamWaitEvent(st, ctx.ecs, 0), "wait");
+  mark(st, "pack_start");
+  if (e == cudaSuccess) {
+    const bool scaled = !strict && !scaled_disabled();
+    rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, dC, dS, (long long)lc, rev, ws, st, scaled)
+                                   : launch_pack<T, false>(g, dC, dS, (long long)lc, rev, ws, st, scaled);
+    mark(st, "kernel_start");
+    if (rc == RS_OK) rc = run_dispatch<T>(g, dA, rev, kind, strict, ws, st, &hs);
+    mark(st, "kernel_end");
+  }
+  // copy-out stream: chunk i leaves once every tile's final unit has released it
+  ck(cudaStreamWaitEvent(ctx.cout, ctx.e0, 0), "wait");
+  for (int i = 0; i < ncw && e == cudaSuccess && rc == RS_OK; ++i) {
+    const CUresult r = ops.wait(reinterpret_cast<CUstream>(ctx.cout), reinterpret_cast<CUdeviceptr>(ctl + 1 + i),
+                                (cuuint32_t)g.tiles, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) {
+      ck(cudaErrorUnknown, "cuStreamWaitValue32");
+      g_err += " (CUresult " + std::to_string((int)r) + ")";
+    }
+    const long long v0 = (long long)i * cw, v1 = v0 + cw < g.len ? v0 + cw : g.len;
+    if (i == 0 || i == ncw - 1) mark(ctx.cout, i == 0 ? "out_first_start" : "out_last_start");
+    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyDeviceToHost, ctx.cout), "A copy-out");
+  }
+  mark(ctx.cout, "out_done");
+  ck(cudaEventRecord(ctx.eend, ctx.cout), "event");
+  ck(cudaStreamWaitEvent(st, ctx.eend, 0), "wait");
+  cudaFreeAsync(mem, st);
+  cudaError_t es = cudaStreamSynchronize(st);
+  if (dbg) {
+    cudaDeviceSynchronize();
+    for (int i = 0; i < nev; ++i) {
+      float ms = 0;
+      const cudaError_t ee = cudaEventElapsedTime(&ms, dev_ev[0], dev_ev[i]);
+      fprintf(stderr, "[rs_apply_host] %-16s %8.3f ms %s\n", ev_name[i], ms, ee == cudaSuccess ? "" : cudaGetErrorString(ee));
+    }
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(dev_ev[i]);
+  }
+  if (rc != RS_OK) return rc;
+  if (e != cudaSuccess) return RS_ECUDA;
+  if (es != cudaSuccess) return fail(RS_ECUDA, std::string("rs_apply_host: ") + cudaGetErrorString(es));
+  return RS_OK;
 }
 
 template <typename T>
@@ -1387,6 +1652,17 @@ rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64
                               int strict, void* workspace, size_t workspace_bytes, void* stream) {
   g_err.clear();
   return apply_packed_impl<float>(A, m, n, lda, k, side, order, kind, strict, workspace, workspace_bytes, stream);
+}
+
+rs_status rs_apply_host_f64(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S,
+                            int64_t ldcs, int64_t k, int side, int order, int kind, int strict, void* stream) {
+  g_err.clear();
+  return apply_host_impl<double>(A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, stream);
+}
+rs_status rs_apply_host_f32(float* A, int64_t m, int64_t n, int64_t lda, const float* C, const float* S,
+                            int64_t ldcs, int64_t k, int side, int order, int kind, int strict, void* stream) {
+  g_err.clear();
+  return apply_host_impl<float>(A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, stream);
 }
 
 rs_status rs_debug_set_trace(void* device_ptr) {

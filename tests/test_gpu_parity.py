@@ -314,3 +314,45 @@ def test_kernels_really_launch(cuda):
     n0 = _lib.launch_count()
     _gpu(A0, seq.C, seq.S)
     assert _lib.launch_count() - n0 == 2  # pack + pipeline
+
+
+@pytest.mark.parametrize("chunks", ("1", "3", "8", "64"))
+@pytest.mark.parametrize("side,order", SIDES_ORDERS)
+def test_host_streaming_entry_point_bitwise(cuda, oracle_mod, monkeypatch, chunks, side, order):
+    """rs_apply_host_* (copy-in / compute / copy-out overlapped in wave-column chunks):
+    bit-identical to the oracle for any chunking, on strided host views (lda > m)."""
+    from paper_2412_01852_b200 import apply_host, generate_sequence, make_inputs
+
+    monkeypatch.setenv("RS_HOST_CHUNKS", chunks)
+    m, n, k = 257, 700, 19
+    A0, seq = make_inputs(m, n, k, 8)
+    if side == "left":
+        seq = generate_sequence(m, k, 6)
+    big = np.asfortranarray(np.zeros((m + 9, n)))
+    view = big[3:3 + m, :]
+    view[...] = A0
+    ref = A0.copy(order="F")
+    oracle_mod.apply_naive(ref, seq.C, seq.S, side=side, order=order)
+    apply_host(view, seq, side=side, order=order)
+    assert_bitwise(ref, view, f"chunks={chunks} {side} {order}")
+    assert not big[:3].any() and not big[3 + m:].any()  # rows outside the view untouched
+
+
+def test_host_streaming_pinned_tensors_and_fp32(cuda, oracle_mod):
+    import torch
+    from paper_2412_01852_b200 import apply_host, compare, make_inputs
+
+    m, n, k = 300, 520, 33
+    A0, seq = make_inputs(m, n, k, 9)
+    hA = torch.empty_strided((m, n), (1, m), dtype=torch.float64, pin_memory=True)
+    hA.copy_(torch.from_numpy(A0))
+    hC = torch.from_numpy(np.asfortranarray(seq.C)).pin_memory()
+    hS = torch.from_numpy(np.asfortranarray(seq.S)).pin_memory()
+    ref = A0.copy(order="F")
+    oracle_mod.apply_naive(ref, seq.C, seq.S)
+    apply_host(hA, (hC, hS), fast=True)
+    assert compare(ref, hA.numpy(), "baseline", k=k).passed
+    A32 = np.asfortranarray(A0.astype(np.float32))
+    apply_host(A32, (seq.C.astype(np.float32), seq.S.astype(np.float32)), fast=True)
+    ref32 = oracle_mod.upcast_reference(A0.astype(np.float32), seq.C.astype(np.float32), seq.S.astype(np.float32))
+    assert np.linalg.norm(A32 - ref32) / np.linalg.norm(ref32) <= 10 * k * np.finfo(np.float32).eps
