@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
     mbar_init(bw + S + 2, 1);
   }
   __syncthreads();
-  // fast fp64: the scaled form, unless the pack found coefficients outside its safe range
-  if constexpr (!STRICT && sizeof(T) == 8) {
+  // fast mode: the scaled form, unless the pack found coefficients outside its safe range
+  if constexpr (!STRICT) {
     if (P.use_scaled && *P.unsafe == 0u) {
       pipeline_units<T, K, R, STRICT, REFL, true>(P, smem_raw);
       return;
@@ -820,10 +820,11 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
   constexpr int K = kK;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= len) return;
-  auto coef = [&](int jj, int p, T& c, T& s) {  // forward-form (c, s) of rotation (jj, p)
+  // scales and taus are formed in fp64 (for fp32 too) and rounded once when stored
+  auto coef = [&](int jj, int p, double& c, double& s) {  // forward-form (c, s) of rotation (jj, p)
     const long long jr = rev ? (long long)(len - 2 - jj) : (long long)jj;
-    c = C[jr + (long long)p * ldcs];
-    s = Sm[jr + (long long)p * ldcs];
+    c = (double)C[jr + (long long)p * ldcs];
+    s = (double)Sm[jr + (long long)p * ldcs];
     if (rev) {
       if constexpr (REFL) {
         c = -c;
@@ -832,7 +833,9 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
       }
     }
   };
-  const T lo = 0x1p-256, hi = 0x1p256;
+  // safe range of scales / taus: |x~| = |x| / sigma stays far from overflow
+  // (fp64: |A| < 2^700; fp32: |A| < 2^60) and no tau overflows the working type
+  const double lo = sizeof(T) == 8 ? 0x1p-256 : 0x1p-60, hi = sizeof(T) == 8 ? 0x1p256 : 0x1p60;
   for (int row = blockIdx.y; row < nparts * (ua + 1); row += gridDim.y) {
     const int part = row / (ua + 1);
     const int i = row - part * (ua + 1);  // unit index within the tile
@@ -843,26 +846,26 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     const int brec = kb * (K + 1) + kScaleRecs;
     SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
                       (size_t)i * nblk * kScaleRecs;
-    T sa = 1, sb = 1;  // running scales of columns j and j+1
+    double sa = 1, sb = 1;  // running scales of columns j and j+1
     bool bad = false;
     for (int l = 0; l < kb; ++l) {
       const int p = p0 + l;
-      T c, s;
+      double c, s;
       if (j >= 1) {  // rotation (j-1, p) touched column j as its y
         coef(j - 1, p, c, s);
         sa *= REFL ? -c : c;
       }
       if (j <= len - 2) {
         coef(j, p, c, s);
-        const T t1 = s * sb / (c * sa);
-        const T t2 = s * sa / (c * sb);
-        bad |= !(c != T(0)) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
+        const double t1 = s * sb / (c * sa);
+        const double t2 = s * sa / (c * sb);
+        bad |= !(c != 0.0) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
         // rotation (j, p) runs in block b at wave u with b(K+1) + u = j + 1 + l
         const int bu = j + 1 + l;
         const int b = bu / (K + 1), u = bu - b * (K + 1);
         SCoef<T> rec{};
-        rec.c = t1;
-        rec.s = -t2;
+        rec.c = (T)t1;
+        rec.s = (T)-t2;
         ubase[(size_t)b * brec + u * kb + l] = rec;
         sa *= c;
         sb *= REFL ? -c : c;
@@ -875,7 +878,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     }
     // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
     const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
-    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)kb * (K + 1))[ue] = sa;
+    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)kb * (K + 1))[ue] = (T)sa;
     if (bad) atomicOr(unsafe, 1u);
   }
 }
@@ -1068,7 +1071,7 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   rs_pack_kernel<T, REFL><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk,
                                                                              lp.ua, nparts, rev);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  if constexpr (sizeof(T) == 8) {
+  {
     if (scaled) {
     unsigned char* base = reinterpret_cast<unsigned char*>(ws);
     uint32_t* unsafe = reinterpret_cast<uint32_t*>(base + g.coef_bytes + g.flags_only);
@@ -1096,7 +1099,7 @@ bool scaled_disabled() {
 template <typename T, bool STRICT, bool REFL>
 rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_t st,
                      const HostStream* hs = nullptr) {
-  const int use_scaled = (!STRICT && sizeof(T) == 8 && !scaled_disabled()) ? 1 : 0;
+  const int use_scaled = (!STRICT && !scaled_disabled()) ? 1 : 0;
   using CoefT = Coef<T, REFL>;
   LaunchPlan lp;
   rs_status rc = plan_launch(g, sizeof(T), &lp);
