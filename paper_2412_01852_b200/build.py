@@ -3,6 +3,12 @@
 The .so is written next to this file so it travels with the repo snapshot to
 the GPU box (a JIT cache under ~/.cache would not). Flags follow the B200
 profiling recipe: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3.
+
+Translation units (compiled in parallel, then linked with the static CUDA runtime):
+
+* ``csrc/rotseq_b200.cu``       host side, C-ABI, pack / naive / peak kernels;
+* ``csrc/pipeline_variant.cu``  compiled 8 times, once per pipeline-kernel family
+  (fp64/fp32 x strict/fast x rotation/reflector).
 """
 
 from __future__ import annotations
@@ -11,20 +17,21 @@ import os
 import shutil
 import subprocess
 import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "rotseq_b200.cu")
+CSRC = os.path.join(HERE, "csrc")
+SRC = os.path.join(CSRC, "rotseq_b200.cu")
+VARIANT_SRC = os.path.join(CSRC, "pipeline_variant.cu")
+DEVICE_HDR = os.path.join(CSRC, "rotseq_device.cuh")
 HDR = os.path.join(ROOT, "include", "rotseq_b200.h")
 OUT = os.path.join(HERE, "librotseq_b200.so")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-cudart", "static",
-    "-Xptxas", "-v",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+
+VARIANTS = [(t, s, r) for t in ("double", "float") for s in (0, 1) for r in (0, 1)]
 
 
 def nvcc_path() -> str:
@@ -41,24 +48,47 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale(OUT, [SRC, HDR, __file__]):
-        return OUT
-    fd, tmp = tempfile.mkstemp(suffix=".so", dir=HERE)
-    os.close(fd)
-    extra = os.environ.get("RS_NVCC_EXTRA", "").split()
-    cmd = [nvcc_path(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", tmp, SRC]
+def _run(cmd):
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
-        os.unlink(tmp)
         raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{' '.join(cmd)}\n{proc.stdout}\n{proc.stderr}")
+    return proc.stderr
+
+
+def build_library(force: bool = False, verbose: bool = False, out: str | None = None, extra=None) -> str:
+    """Compile (in parallel) and link the library. ``out``/``extra`` build developer
+    variants (e.g. ``extra=["-DRS_TRACE"]``) without touching the product .so."""
+    out = out or OUT
+    deps = [SRC, VARIANT_SRC, DEVICE_HDR, HDR, __file__]
+    if not force and extra is None and not _stale(out, deps):
+        return out
+    extra = list(extra or []) + os.environ.get("RS_NVCC_EXTRA", "").split()
+    nvcc = nvcc_path()
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    tmpdir = tempfile.mkdtemp(prefix="rs_build_", dir=HERE)
+    try:
+        jobs = [(os.path.join(tmpdir, "host.o"), [nvcc, *NVCC_FLAGS, *extra, *inc, "-c", "-o",
+                                                   os.path.join(tmpdir, "host.o"), SRC])]
+        for t, s, r in VARIANTS:
+            obj = os.path.join(tmpdir, f"pipe_{t}_{s}_{r}.o")
+            jobs.append((obj, [nvcc, *NVCC_FLAGS, *extra, *inc, f"-DRS_VARIANT_T={t}", f"-DRS_VARIANT_STRICT={s}",
+                               f"-DRS_VARIANT_REFL={r}", "-c", "-o", obj, VARIANT_SRC]))
+        with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
+            logs = list(pool.map(lambda j: _run(j[1]), jobs))
+        fd, tmp = tempfile.mkstemp(suffix=".so", dir=os.path.dirname(out))
+        os.close(fd)
+        _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[j[0] for j in jobs]])
+        os.replace(tmp, out)
+    finally:
+        shutil.rmtree(tmpdir, ignore_errors=True)
+    info = "\n".join(logs)
     if verbose:
-        print(proc.stderr)
-    os.replace(tmp, OUT)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(proc.stderr)
-    return OUT
+        print(info)
+    if out == OUT:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(info)
+    return out
 
 
 if __name__ == "__main__":
-    print(build_library(force=True, verbose=True))
+    print(build_library(force=True, verbose=False))

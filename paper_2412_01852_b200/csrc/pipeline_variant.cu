@@ -1,0 +1,36 @@
+// pipeline_variant.cu — one pipeline-kernel family per compilation: build.py compiles
+// this file once per (RS_VARIANT_T, RS_VARIANT_STRICT, RS_VARIANT_REFL) so the eight
+// fully unrolled kernel families (each with its resident and host-streaming variant)
+// build in parallel. The launcher opts the kernel in to the device's full dynamic shared
+// memory once per device and launches it (cooperative: all CTAs co-resident).
+#include "rotseq_device.cuh"
+
+#if !defined(RS_VARIANT_T) || !defined(RS_VARIANT_STRICT) || !defined(RS_VARIANT_REFL)
+#error "compile with -DRS_VARIANT_T=double|float -DRS_VARIANT_STRICT=0|1 -DRS_VARIANT_REFL=0|1"
+#endif
+
+namespace rsk {
+
+template <typename T, bool STRICT, bool REFL, bool HS>
+cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) {
+  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL, HS>;
+  static std::atomic<int> configured{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int bit = 1 << (dev & 31);
+  if (!(configured.load(std::memory_order_relaxed) & bit)) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit, std::memory_order_relaxed);
+  }
+  return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, false>(
+    const cudaLaunchConfig_t&, const PipeParams&);
+template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, true>(
+    const cudaLaunchConfig_t&, const PipeParams&);
+
+}  // namespace rsk

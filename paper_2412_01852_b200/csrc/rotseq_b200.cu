@@ -47,888 +47,21 @@
 #include <type_traits>
 
 #include "rotseq_b200.h"
+#include "rotseq_device.cuh"
 
 #define RS_VERSION 10300
 
 namespace {
 
-// ------------------------------------------------------------------------------------
-// compile-time geometry
-// ------------------------------------------------------------------------------------
-constexpr int kK = 8;          // max sweeps per unit (lanes of the wavefront)
-constexpr int kR = 2;          // owners (rows) per thread
-#ifndef RS_FLAG_EVERY
-#define RS_FLAG_EVERY 8
-#endif
-#ifndef RS_STAGES
-#define RS_STAGES 2
-#endif
-constexpr int kStages = RS_STAGES;  // ring depth in chunks of K+1 columns (self-fill runs S-1 ahead)
-constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
-constexpr int kTileOwners = 32 * kR;
-constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
-constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
-constexpr int kFlagEvery = RS_FLAG_EVERY;   // hand-off progress is published every 8 blocks (fence cost)
-constexpr size_t kTrashBytes = 32 * kR * 8;  // scratch slot per lane for rows past the matrix
-
-enum : int { SRC_RING = 0, SRC_GLOBAL = 1, SRC_FLAG = 2 };
-enum : int { DST_RING = 0, DST_GLOBAL = 1, DST_FLAG = 2 };
+using namespace rsk;
 
 std::atomic<long long> g_launches{0};
 thread_local std::string g_err;
+unsigned long long* g_trace_buf = nullptr;  // rs_debug_set_trace (RS_TRACE builds)
 
 rs_status fail(rs_status st, const std::string& msg) {
   g_err = msg;
   return st;
-}
-
-// ------------------------------------------------------------------------------------
-// coefficient records and arithmetic
-// ------------------------------------------------------------------------------------
-template <typename T, bool REFL>
-struct Coef;
-template <>
-struct alignas(16) Coef<double, false> {
-  double c, s;
-};
-template <>
-struct alignas(16) Coef<float, false> {
-  float c, s, pad0, pad1;  // 16-byte records: bulk-copy granularity, one LDS.128
-};
-template <typename T>
-struct alignas(4 * sizeof(T)) Coef<T, true> {
-  T s, d, e, pad;  // d = c - s, e = c + s (hoisted exactly as core.py:142-143)
-};
-// Scaled ("fast Givens") records: (tau1, -tau2), see rs_pack_scaled_kernel.
-template <typename T>
-using SCoef = Coef<T, false>;
-constexpr int kScaleRecs = 5;  // per block: K+1 = 9 column scales (fp64) in 5 16-byte records
-
-// bytes of one per-warp coefficient buffer (two per warp: double buffering)
-template <typename T, bool REFL>
-__host__ __device__ constexpr size_t coef_buf_bytes() {
-  const size_t std_bytes = (size_t)(kK + 1) * kK * sizeof(Coef<T, REFL>);
-  const size_t scl_bytes = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
-  return std_bytes > scl_bytes ? std_bytes : scl_bytes;
-}
-
-__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
-__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
-__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-
-// Rotation (core.py:130-137):   x' = c*x + s*y ; y' = c*y - s*x
-// Reflector (core.py:140-149):  w = s*(x+y) ; x' = w + d*x ; y' = w - e*y
-template <typename T, bool STRICT>
-__device__ __forceinline__ void rot2(T& x, T& y, T c, T s) {
-  if constexpr (STRICT) {
-    const T nx = add_rn(mul_rn(c, x), mul_rn(s, y));
-    const T ny = sub_rn(mul_rn(c, y), mul_rn(s, x));
-    x = nx;
-    y = ny;
-  } else {
-    const T cx = mul_rn(c, x);
-    const T sx = mul_rn(s, x);
-    x = fma_rn(s, y, cx);
-    y = fma_rn(c, y, -sx);
-  }
-}
-template <typename T, bool STRICT>
-__device__ __forceinline__ void refl2(T& x, T& y, T s, T d, T e) {
-  const T w = mul_rn(s, add_rn(x, y));
-  if constexpr (STRICT) {
-    x = add_rn(w, mul_rn(d, x));
-    y = sub_rn(w, mul_rn(e, y));
-  } else {
-    x = fma_rn(d, x, w);
-    y = fma_rn(-e, y, w);
-  }
-}
-// Scaled form (fast mode): the window holds x~ = x / sigma_x per column; one rotation is
-//   x~' = x~ + tau1 * y~ ,  y~' = y~ - tau2 * x~      (2 FMAs instead of 2 MUL + 2 FMA)
-template <typename T>
-__device__ __forceinline__ void xform_scaled(T& x, T& y, const SCoef<T>& cf) {
-  const T xo = x;
-  x = fma_rn(cf.c, y, x);
-  y = fma_rn(cf.s, xo, y);
-}
-template <typename T, bool STRICT, bool REFL>
-__device__ __forceinline__ void xform(T& x, T& y, const Coef<T, REFL>& cf) {
-  if constexpr (REFL) {
-    refl2<T, STRICT>(x, y, cf.s, cf.d, cf.e);
-  } else {
-    rot2<T, STRICT>(x, y, cf.c, cf.s);
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// PTX helpers: mbarrier, bulk copy, flags
-// ------------------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// The suspend-time hint parks a waiting warp in hardware until the phase completes instead
-// of spinning: spinning waits would steal issue slots from the warps sharing its SM
-// sub-partition (measured: ~14% of all issued instructions without the hint).
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "RS_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra RS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(kSuspendHintNs)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-// TMA bulk copy global -> shared completing `bytes` of transaction count on `bar`.
-__device__ __forceinline__ void bulk_g2s_nowait(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-// cp.async (LDGSTS) of one element; src_size 0 zero-fills (out-of-range rows/columns).
-template <typename T>
-__device__ __forceinline__ void cp_async_elem(T* dst, const T* src, bool valid) {
-  if constexpr (sizeof(T) == 8) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "r"(valid ? 8 : 0)
-                 : "memory");
-  } else {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
-                 "r"(valid ? 4 : 0)
-                 : "memory");
-  }
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
-  while (ld_acquire_shared(p) < target) __nanosleep(32);
-}
-__device__ __forceinline__ uint32_t wait_flag(const uint32_t* p, uint32_t target) {
-  uint32_t v;
-  while ((v = ld_acquire(p)) < target) __nanosleep(64);
-  return v;
-}
-
-// Debug-only instrumentation (compiled in with -DRS_TRACE; see rs_debug_set_trace).
-// Each unit a warp runs writes one record of kTraceWords uint64 to
-// g_trace[((cta * kMaxWarps + warp) * kTraceRounds + round) * kTraceWords]:
-//   0 tile | src<<40 | dst<<44 | smid<<48, 1 globaltimer at unit start, 2 at unit end,
-//   3 cycles issuing self-fill / waiting for progress flags, 4 coefficient waits, 5 ring-full
-//   waits, 6 ring-space waits, 7 compute (run_block), 8 post-block hand-off work, 9 p0 | kb<<32.
-constexpr int kTraceWords = 10;
-constexpr int kTraceRounds = 32;
-__device__ unsigned long long* g_trace = nullptr;
-#ifdef RS_TRACE
-__device__ __forceinline__ unsigned long long trace_clock() { return clock64(); }
-__device__ __forceinline__ unsigned long long trace_gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ unsigned trace_smid() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
-}
-#else
-__device__ __forceinline__ unsigned long long trace_clock() { return 0; }
-__device__ __forceinline__ unsigned long long trace_gtime() { return 0; }
-__device__ __forceinline__ unsigned trace_smid() { return 0; }
-#endif
-struct TraceAcc {
-  unsigned long long t0 = 0, c[6] = {0, 0, 0, 0, 0, 0};
-};
-__device__ __forceinline__ void trace_unit(int warp, int jr, long long tile, int p0, int kb, int src, int dst,
-                                           const TraceAcc& acc) {
-#ifdef RS_TRACE
-  unsigned long long* t = g_trace;
-  if (t != nullptr && (threadIdx.x & 31) == 0 && jr < kTraceRounds) {
-    unsigned long long* rec = t + (((size_t)blockIdx.x * kMaxWarps + warp) * kTraceRounds + jr) * kTraceWords;
-    rec[0] = (unsigned long long)tile | ((unsigned long long)src << 40) | ((unsigned long long)dst << 44) |
-             ((unsigned long long)trace_smid() << 48);
-    rec[1] = acc.t0;
-    rec[2] = trace_gtime();
-    for (int i = 0; i < 6; ++i) rec[3 + i] = acc.c[i];
-    rec[9] = (unsigned long long)p0 | ((unsigned long long)kb << 32);
-  }
-#else
-  (void)warp, (void)jr, (void)tile, (void)p0, (void)kb, (void)src, (void)dst, (void)acc;
-#endif
-}
-
-// ------------------------------------------------------------------------------------
-// kernel parameters
-// ------------------------------------------------------------------------------------
-struct PipeParams {
-  void* A;           // element (owner o, wave-column v) at A + o*os + v*cs
-  long long os;      // owner stride (elements)
-  long long cs;      // wave-column stride (elements, negative for reverse order)
-  long long owners;  // independent lines (rows for right side, columns for left)
-  long long tiles;   // ceil(owners / 64)
-  long long units;   // U: (tile, sweep-range) units in total
-  long long t1;      // the first t1 tiles hold ua+1 units, the others ua
-  const void* coef;  // packed coefficient blocks (see rs_pack_kernel)
-  const void* coef_scaled;  // scaled-form blocks (rs_pack_scaled_kernel)
-  const uint32_t* unsafe;   // set by rs_pack_scaled_kernel: scaled form out of safe range
-  uint32_t* flags;   // [tiles*k + 1] progress flags of in-place hand-offs, index tile*k + p0
-  void* trash;       // 32*R elements: write/read target of lanes past the last row
-  int ua;            // units per tile (base)
-  int len;           // length of the rotated dimension (n right, m left)
-  int k;             // sweeps
-  int nchunk;        // ceil(len / (K+1))
-  int nblk;          // nchunk + 1
-  int nw;            // warps per CTA (multiple of 4)
-  int use_scaled;    // fast fp64: scaled records were packed
-  int credit;        // ring credit in chunks (1..S)
-  // host-streaming mode (rs_apply_host_*): A arrives from the host in wave-column chunks
-  // of cw columns while the kernel runs, and leaves in the same chunks as soon as every
-  // tile's final unit has emitted them. Null pointers: A is resident.
-  const uint32_t* arrived;  // number of chunks already copied in (written by the copy stream)
-  uint32_t* done;           // per chunk: tiles whose final unit has emitted it
-  int cw;                   // chunk width in wave columns
-  int ncw;                  // number of chunks
-};
-
-// ------------------------------------------------------------------------------------
-// work split. The U units are numbered tile-major; tile t holds u_t = ua (+1 for t < t1)
-// units whose sweep ranges split the k sweeps evenly: unit i of the tile covers sweeps
-// [floor(i*k/u_t), floor((i+1)*k/u_t)) (width <= K). The planner picks U = 4*G*q so every
-// CTA runs 4q consecutive units and, with position p on warp p % NW (NW a multiple of 4),
-// every SM sub-partition runs q units of nearly equal total width.
-// ------------------------------------------------------------------------------------
-struct Unit {
-  long long tile;
-  int p0;  // first sweep
-  int kb;  // sweeps (1..kK)
-};
-__host__ __device__ __forceinline__ long long tile_first_unit(long long t, long long t1, int ua) {
-  return t < t1 ? t * (ua + 1) : t1 * (ua + 1) + (t - t1) * ua;
-}
-__host__ __device__ __forceinline__ Unit unit_at(long long g, long long t1, int ua, int k) {
-  Unit u;
-  const long long big = t1 * (ua + 1);
-  long long i;
-  int ut;
-  if (g < big) {
-    u.tile = g / (ua + 1);
-    i = g - u.tile * (ua + 1);
-    ut = ua + 1;
-  } else {
-    const long long r = g - big;
-    u.tile = t1 + r / ua;
-    i = r - (u.tile - t1) * ua;
-    ut = ua;
-  }
-  u.p0 = (int)(i * k / ut);
-  u.kb = (int)((i + 1) * k / ut) - u.p0;
-  return u;
-}
-// CTA c runs units [g0, g1). When the range ends inside a tile whose first unit lies inside
-// the range, that last partial tile (it feeds the next CTA) runs first: nl > 0 units.
-struct CtaRange {
-  long long g0, g1;
-  int nl;
-};
-__host__ __device__ __forceinline__ CtaRange cta_range(long long U, long long c, long long G, long long t1, int ua,
-                                                       int k) {
-  CtaRange r;
-  r.g0 = U * c / G;
-  r.g1 = U * (c + 1) / G;
-  r.nl = 0;
-  if (r.g1 > r.g0) {
-    const Unit last = unit_at(r.g1 - 1, t1, ua, k);
-    if (last.p0 + last.kb < k) {
-      const long long f = tile_first_unit(last.tile, t1, ua);
-      if (f > r.g0) r.nl = (int)(r.g1 - f);
-    }
-  }
-  return r;
-}
-__host__ __device__ __forceinline__ long long pos_to_unit(const CtaRange& r, long long p) {
-  return p < r.nl ? r.g1 - r.nl + p : r.g0 + p - r.nl;
-}
-__host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, long long g) {
-  return g >= r.g1 - r.nl ? g - (r.g1 - r.nl) : g - r.g0 + r.nl;
-}
-
-// ------------------------------------------------------------------------------------
-// one block of K+1 waves for one warp (fully unrolled; window slots are compile-time)
-//   block b covers waves t = b(K+1)-1 .. b(K+1)+K-1. At the start of wave u it emits
-//   column (b-1)(K+1)+u (finished after wave t-1) through the output pointers, then loads
-//   column b(K+1)+u into slot u; lane l < KB rotates columns (t-l, t-l+1) = slots
-//   (u-1-l, u-l) with record cb[u*KB+l]. Output goes to the next unit's ring (shared)
-//   or to A (global) through one generic store path, so a unit width compiles to ONE loop
-//   body (instruction-cache footprint). EDGE blocks check every column and lane at run time.
-// ------------------------------------------------------------------------------------
-template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED>
-__device__ __forceinline__ void run_block(T (&w)[R][K + 1],
-                                          const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
-                                          const T* __restrict__ islot, T* const (&op)[R], const long long (&ostr)[R],
-                                          int b, int len, int Kb, int lane, bool has_in_rt, bool has_out_rt) {
-  constexpr int TR = 32 * R;
-  constexpr int NL = EDGE ? K : KB;
-  const long long c0 = (long long)b * (K + 1);
-  const bool has_in = !EDGE || has_in_rt;
-  const bool has_out = !EDGE || has_out_rt;
-  // scaled mode: the emitted column is multiplied back by its scale (after the block's records)
-  const T* __restrict__ sc = reinterpret_cast<const T*>(cb + (K + 1) * (EDGE ? Kb : KB));
-  T* q[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) q[r] = op[r];
-#pragma unroll
-  for (int u = 0; u <= K; ++u) {
-    if (has_out) {
-      const long long col = c0 - (K + 1) + u;
-      if (!EDGE || col < len) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if constexpr (SCALED) {
-            *q[r] = mul_rn(w[r][u], sc[u]);
-          } else {
-            *q[r] = w[r][u];
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) q[r] += ostr[r];
-    }
-    {
-      const long long col = c0 + u;
-      if (!EDGE || (has_in && col < len)) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) w[r][u] = islot[u * TR + lane + 32 * r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) w[r][u] = T(0);
-      }
-    }
-#pragma unroll
-    for (int l = 0; l < NL; ++l) {
-      constexpr int M = K + 1;
-      const int sx = (u - 1 - l + 2 * M) % M;
-      const int sy = (sx + 1) % M;
-      if (EDGE) {
-        const long long j = c0 + u - 1 - l;
-        if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
-      }
-      const auto cf = cb[u * (EDGE ? Kb : KB) + l];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if constexpr (SCALED) {
-          xform_scaled<T>(w[r][sx], w[r][sy], cf);
-        } else {
-          xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
-        }
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// the persistent pipeline kernel
-// ------------------------------------------------------------------------------------
-template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED>
-__device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned char* smem_raw) {
-  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
-  constexpr int TR = 32 * R;
-  constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
-  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
-  constexpr int S = kStages;
-  constexpr int FA = S - 1;  // self-fill distance in chunks
-  static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
-  constexpr int NBAR = kCtlWords;
-
-  const int NW = P.nw;
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
-
-  T* const A = reinterpret_cast<T*>(P.A);
-  const int len = P.len;
-  const int k = P.k;
-  const int nchunk = P.nchunk;
-  const int nblk = P.nblk;
-  const uint32_t credit = (uint32_t)P.credit;
-  uint64_t* const bar_in = bars + warp * NBAR;  // in-ring of this warp: full[S], consumed, coef[2]
-  uint64_t* const full_in = bar_in;
-  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
-  uint64_t* const cbar = bar_in + S + 1;
-  // the next position in the same round runs on warp + 1
-  uint64_t* const full_out = bars + (warp + 1) * NBAR;
-  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
-  T* const rin = ring_sm + (size_t)warp * S * CHUNK;
-  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
-  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
-
-  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
-  const long long npos = cr.g1 - cr.g0;
-  uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
-
-  for (int jr = 0;; ++jr) {
-    const long long pos = (long long)jr * NW + warp;
-    if (pos >= npos) break;
-    const long long g = pos_to_unit(cr, pos);
-    const Unit un = unit_at(g, P.t1, P.ua, k);
-    const long long tile = un.tile;
-    const int p0 = un.p0;
-    const int Kb = un.kb;
-    // the producer of this unit is unit g-1 (same tile, ends at sweep p0); its consumer is
-    // g+1. Ring hand-off when that unit is the neighbouring position of the same round.
-    int src = SRC_GLOBAL, dst = DST_GLOBAL;
-    if (p0 > 0) {
-      src = SRC_FLAG;
-      if (warp > 0 && g - 1 >= cr.g0 && unit_to_pos(cr, g - 1) == pos - 1) src = SRC_RING;
-    }
-    if (p0 + Kb < k) {
-      dst = DST_FLAG;
-      if (warp < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
-    }
-    const bool self = src != SRC_RING;
-
-    T* grow[R];        // element (row r, column 0) of this lane's lines
-    long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const long long o = tile * TR + lane + 32 * r;
-      const bool ok = o < P.owners;
-      grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
-      gcs[r] = ok ? P.cs : 0;
-    }
-    // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
-    // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
-    const int part = tile < P.t1 ? 1 : 0;
-    const int brec = Kb * (K + 1) + (SCALED ? kScaleRecs : 0);
-    const CoefT* ubase;
-    if constexpr (SCALED) {
-      const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
-      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
-              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
-    } else {
-      ubase = reinterpret_cast<const CoefT*>(P.coef) + (size_t)part * k * nblk * (K + 1) + (size_t)p0 * nblk * (K + 1);
-    }
-    const uint32_t blk_bytes = (uint32_t)(brec * sizeof(CoefT));
-    // one elected lane: WAR fence for the buffer's previous readers, arm, start the copy
-    auto issue_coef = [&](int b, uint32_t buf) {
-      if (lane == 0) {
-        uint64_t* bar = &cbar[buf];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, blk_bytes);
-        bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
-      }
-    };
-    const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
-    const uint32_t* myflag = P.flags + tile * k + p0;
-    uint32_t* const outflag = P.flags + tile * k + p0 + Kb;
-    TraceAcc tacc;
-    tacc.t0 = trace_gtime();
-
-    issue_coef(0, cseq & 1);
-
-    // self-filled input (sweep 0 reads A; a flag hand-off reads A after the producer's
-    // progress flag): cp.async (LDGSTS) straight into this warp's own ring, FA chunks ahead.
-    uint32_t flag_seen = 0;
-    auto fill_chunk = [&](int q) {
-      if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
-      if (src == SRC_GLOBAL && P.arrived != nullptr) {  // host streaming: wait for the copy
-        long long cend = (long long)q * (K + 1) + K;
-        if (cend > len - 1) cend = len - 1;
-        const uint32_t need = (uint32_t)(cend / P.cw) + 1u;
-        if (flag_seen < need) flag_seen = wait_flag(P.arrived, need);
-      }
-      T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
-      const long long c0 = (long long)q * (K + 1);
-      const T* sp[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) sp[r] = grow[r] + c0 * gcs[r];
-      if (c0 + K < len) {
-#pragma unroll
-        for (int v = 0; v <= K; ++v) {
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            cp_async_elem(dstp + v * TR + lane + 32 * r, sp[r], true);
-            sp[r] += gcs[r];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v <= K; ++v) {
-          const bool cv = c0 + v < len;
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            cp_async_elem(dstp + v * TR + lane + 32 * r, cv ? sp[r] : grow[r], cv);
-            sp[r] += gcs[r];
-          }
-        }
-      }
-      cp_async_commit();
-    };
-    // Self-filled chunks still arrive on full_in (nobody waits on them) so the barrier's
-    // phase count stays equal to the chunk sequence number for ring-fed rounds later on.
-    unsigned long long tc = trace_clock();
-    if (self) {
-      fill_chunk(0);
-      if (FA >= 2 && 1 < nchunk) fill_chunk(1);
-      if (FA >= 2 && 1 < nchunk)
-        cp_async_wait_group<1>();
-      else
-        cp_async_wait_group<0>();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full_in[seq0 % S]);
-    }
-    tacc.c[0] += trace_clock() - tc;
-
-    T w[R][K + 1];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int s = 0; s <= K; ++s) w[r][s] = T(0);
-
-    const bool outring = dst == DST_RING;
-    int done_sig = 0;  // host streaming: chunks already released by this (final) unit
-    // One block: protocol + compute. KB / EDGE are compile-time so the interior loop
-    // carries no per-block branches beyond this unit's hand-off protocol.
-    auto block = [&](int b, auto kb_c, auto edge_c) {
-      constexpr int KB = decltype(kb_c)::value;
-      constexpr bool EDGE = decltype(edge_c)::value;
-      unsigned long long t0 = trace_clock();
-      if (b + 1 < nblk) issue_coef(b + 1, (cseq + 1) & 1);
-      const bool has_in = !EDGE || b < nchunk;
-      const bool has_out = !EDGE || b >= 1;
-      if (self && b + FA < nchunk) fill_chunk(b + FA);
-      unsigned long long t1 = trace_clock();
-      const uint32_t iseq = seq0 + (uint32_t)b;
-      const T* islot = rin + (iseq % S) * CHUNK;
-      const uint32_t oseq = seq0 + (uint32_t)b - 1u;
-      // output pointers: the consumer's ring slot (column stride TR) or A (stride gcs)
-      T* op[R];
-      long long ostr[R];
-      if (outring) {
-        T* oslot = rout + (oseq % S) * CHUNK + lane;
-#pragma unroll
-        for (int r = 0; r < R; ++r) op[r] = oslot + 32 * r, ostr[r] = TR;
-      } else {
-        const long long cb0 = (long long)b * (K + 1) - (K + 1);
-#pragma unroll
-        for (int r = 0; r < R; ++r) op[r] = grow[r] + cb0 * gcs[r], ostr[r] = gcs[r];
-      }
-      mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
-      unsigned long long t2 = trace_clock();
-      if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
-      unsigned long long t3 = trace_clock();
-      // ring credit: the producer runs at most `credit` chunks ahead of its consumer
-      if (outring && has_out && oseq >= credit) wait_count(consumed_out, oseq - credit + 1u);
-      unsigned long long t4 = trace_clock();
-      run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED>(
-          w, reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF), islot, op, ostr, b, len, Kb, lane, b < nchunk,
-          b >= 1);
-      __syncwarp();
-      unsigned long long t5 = trace_clock();
-      if (lane == 0) {
-        if (has_in) st_release_shared(consumed_in, iseq + 1u);
-        if (outring && has_out) mbar_arrive(&full_out[oseq % S]);
-        if (dst == DST_FLAG && has_out && (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
-          // the warp barrier above orders every lane's stores before lane 0's gpu-scope
-          // fence; the release store then publishes "chunks 0..b-1 are in A"
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          st_release(outflag, (uint32_t)b);
-        }
-        if (dst == DST_GLOBAL && has_out && P.done != nullptr) {  // host streaming: release chunks
-          long long e = (long long)b * (K + 1) - 1;  // last column emitted by this block
-          if (e > len - 1) e = len - 1;
-          const int nd = e == len - 1 ? P.ncw : (int)((e + 1) / P.cw);
-          if (nd > done_sig) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            for (; done_sig < nd; ++done_sig) atomicAdd(P.done + done_sig, 1u);
-          }
-        }
-      }
-      if (self && b + 1 < nchunk) {  // the chunk read by the next block has landed
-        if (FA >= 2 && b + 2 < nchunk)
-          cp_async_wait_group<1>();
-        else
-          cp_async_wait_group<0>();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full_in[(iseq + 1u) % S]);
-      }
-      ++cseq;
-      unsigned long long t6 = trace_clock();
-      tacc.c[0] += t1 - t0;
-      tacc.c[1] += t2 - t1;
-      tacc.c[2] += t3 - t2;
-      tacc.c[3] += t4 - t3;
-      tacc.c[4] += t5 - t4;
-      tacc.c[5] += t6 - t5;
-    };
-    using T_ = std::true_type;
-    using F_ = std::false_type;
-    using I8 = std::integral_constant<int, K>;
-    const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
-    const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
-    block(0, I8{}, T_{});
-    switch (Kb) {
-      case 8: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 8>{}, F_{}); break;
-      case 7: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 7>{}, F_{}); break;
-      case 6: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 6>{}, F_{}); break;
-      case 5: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 5>{}, F_{}); break;
-      case 4: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 4>{}, F_{}); break;
-      case 3: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 3>{}, F_{}); break;
-      case 2: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 2>{}, F_{}); break;
-      default: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 1>{}, F_{}); break;
-    }
-    for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
-    trace_unit(warp, jr, tile, p0, Kb, src, dst, tacc);
-  }
-}
-
-template <typename T, int K, int R, bool STRICT, bool REFL>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
-  constexpr int S = kStages;
-  constexpr int NBAR = kCtlWords;
-  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int NW = P.nw;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * CBUF + (size_t)NW * S * (K + 1) * 32 * R * sizeof(T));
-  // "full" is alias-safe as an mbarrier (the consumer has always seen chunk seq-S before it
-  // waits for seq); "consumed" is a monotonic counter because a ring's producer changes
-  // between rounds (previous warp vs. self-fill), which a parity test cannot express.
-  if (threadIdx.x < NW) {
-    uint64_t* bw = bars + threadIdx.x * NBAR;
-#pragma unroll
-    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
-    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
-    mbar_init(bw + S + 1, 1);
-    mbar_init(bw + S + 2, 1);
-  }
-  __syncthreads();
-  // fast mode: the scaled form, unless the pack found coefficients outside its safe range
-  if constexpr (!STRICT) {
-    if (P.use_scaled && *P.unsafe == 0u) {
-      pipeline_units<T, K, R, STRICT, REFL, true>(P, smem_raw);
-      return;
-    }
-  }
-  pipeline_units<T, K, R, STRICT, REFL, false>(P, smem_raw);
-}
-
-// ------------------------------------------------------------------------------------
-// coefficient repack: C/S (len-1) x k column-major -> per-unit blocks. For each sweep
-// partition (part 0: ua units per tile, part 1: ua+1), unit i (sweeps p0..p0+kb-1) owns
-// nblk blocks of (K+1) x kb records at record offset part*k*nblk*(K+1) + p0*nblk*(K+1):
-// block b, wave u, lane l holds rotation (j = b(K+1)+u-1-l, p0+l), zero outside
-// 0 <= j <= len-2 — the GPU analogue of the reference's per-window coefficient gather
-// (blocking.py:364-373). One bulk copy stages a block. Reverse order mirrors j and
-// negates S (rotation) or C (reflector): both exact in IEEE arithmetic.
-// ------------------------------------------------------------------------------------
-template <typename T, bool REFL>
-__global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
-                                                      const T* __restrict__ Sm, long long ldcs, int len, int k,
-                                                      int nblk, int ua, int nparts, int rev) {
-  constexpr int K = kK;
-  const int per_p = nblk * (K + 1);
-  for (int row = blockIdx.y; row < nparts * k; row += gridDim.y) {
-    const int part = row / k;
-    const int p = row - part * k;
-    const int ut = ua + part;
-    // unit i of this partition holding sweep p: p0(i) = floor(i*k/ut)
-    int i = (int)(((long long)p * ut) / k);
-    while (i + 1 < ut && (int)(((long long)(i + 1) * k) / ut) <= p) ++i;
-    while (i > 0 && (int)(((long long)i * k) / ut) > p) --i;
-    const int p0 = (int)(((long long)i * k) / ut);
-    const int kb = (int)(((long long)(i + 1) * k) / ut) - p0;
-    const int l = p - p0;
-    Coef<T, REFL>* dst = out + (size_t)part * k * per_p + (size_t)p0 * per_p + l;
-    for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < per_p; x += gridDim.x * blockDim.x) {
-      const int b = x / (K + 1);
-      const int u = x - b * (K + 1);
-      const long long j = (long long)b * (K + 1) + u - 1 - l;
-      Coef<T, REFL> cf{};
-      if (j >= 0 && j <= len - 2) {
-        const long long jj = rev ? (long long)(len - 2) - j : j;
-        T c = __ldg(C + jj + (long long)p * ldcs);
-        T s = __ldg(Sm + jj + (long long)p * ldcs);
-        if constexpr (REFL) {
-          if (rev) c = -c;
-          cf.s = s;
-          cf.d = c - s;
-          cf.e = c + s;
-        } else {
-          if (rev) s = -s;
-          cf.c = c;
-          cf.s = s;
-        }
-      }
-      dst[((size_t)b * (K + 1) + u) * kb] = cf;
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// scaled ("fast Givens") repack for fast-mode fp64. Inside a unit every column j carries a
-// scale sigma_j (1 at unit entry) and the window holds x~ = x / sigma. With (c, s) in
-// forward form, rotation (j, p) is
-//   x' = c*x + s*y = c*sx * (x~ + tau1*y~),  tau1 = s*sy / (c*sx),   sx' = c*sx
-//   y' = c*y - s*x = c*sy * (y~ - tau2*x~),  tau2 = s*sx / (c*sy),   sy' = c*sy
-// (reflector: y' = s*x - c*y, same taus, sy' = -c*sy), i.e. 2 FMAs instead of 2 MUL +
-// 2 FMA. The scales depend only on C/S, so they are computed here, once per call:
-// thread (partition, unit, column j) walks the unit's sweeps in application order
-// (rotation (j-1, p) before (j, p) before (j+1, p)). The column's final scale is applied
-// when the kernel emits it. Records: (tau1, -tau2) at [b][u*kb + l] as in rs_pack_kernel,
-// then the K+1 emission scales of the block. A coefficient that would push a scale or tau
-// outside [2^-256, 2^256] (or c == 0) sets *unsafe and the kernel uses the standard form.
-// ------------------------------------------------------------------------------------
-template <typename T, bool REFL>
-__global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restrict__ out, const T* __restrict__ C,
-                                                             const T* __restrict__ Sm, long long ldcs, int len, int k,
-                                                             int nblk, int ua, int nparts, int rev,
-                                                             uint32_t* __restrict__ unsafe) {
-  constexpr int K = kK;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= len) return;
-  // scales and taus are formed in fp64 (for fp32 too) and rounded once when stored
-  auto coef = [&](int jj, int p, double& c, double& s) {  // forward-form (c, s) of rotation (jj, p)
-    const long long jr = rev ? (long long)(len - 2 - jj) : (long long)jj;
-    c = (double)C[jr + (long long)p * ldcs];
-    s = (double)Sm[jr + (long long)p * ldcs];
-    if (rev) {
-      if constexpr (REFL) {
-        c = -c;
-      } else {
-        s = -s;
-      }
-    }
-  };
-  // safe range of scales / taus: |x~| = |x| / sigma stays far from overflow
-  // (fp64: |A| < 2^700; fp32: |A| < 2^60) and no tau overflows the working type
-  const double lo = sizeof(T) == 8 ? 0x1p-256 : 0x1p-60, hi = sizeof(T) == 8 ? 0x1p256 : 0x1p60;
-  for (int row = blockIdx.y; row < nparts * (ua + 1); row += gridDim.y) {
-    const int part = row / (ua + 1);
-    const int i = row - part * (ua + 1);  // unit index within the tile
-    const int ut = ua + part;
-    if (i >= ut) continue;
-    const int p0 = (int)(((long long)i * k) / ut);
-    const int kb = (int)(((long long)(i + 1) * k) / ut) - p0;
-    const int brec = kb * (K + 1) + kScaleRecs;
-    SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
-                      (size_t)i * nblk * kScaleRecs;
-    double sa = 1, sb = 1;  // running scales of columns j and j+1
-    bool bad = false;
-    for (int l = 0; l < kb; ++l) {
-      const int p = p0 + l;
-      double c, s;
-      if (j >= 1) {  // rotation (j-1, p) touched column j as its y
-        coef(j - 1, p, c, s);
-        sa *= REFL ? -c : c;
-      }
-      if (j <= len - 2) {
-        coef(j, p, c, s);
-        const double t1 = s * sb / (c * sa);
-        const double t2 = s * sa / (c * sb);
-        bad |= !(c != 0.0) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
-        // rotation (j, p) runs in block b at wave u with b(K+1) + u = j + 1 + l
-        const int bu = j + 1 + l;
-        const int b = bu / (K + 1), u = bu - b * (K + 1);
-        SCoef<T> rec{};
-        rec.c = (T)t1;
-        rec.s = (T)-t2;
-        ubase[(size_t)b * brec + u * kb + l] = rec;
-        sa *= c;
-        sb *= REFL ? -c : c;
-        if (j + 1 <= len - 2) {  // rotation (j+1, p) touches column j+1 as its x
-          coef(j + 1, p, c, s);
-          sb *= c;
-        }
-      }
-      bad |= !(fabs(sa) >= lo && fabs(sa) <= hi) || !(fabs(sb) >= lo && fabs(sb) <= hi);
-    }
-    // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
-    const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
-    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)kb * (K + 1))[ue] = (T)sa;
-    if (bad) atomicOr(unsafe, 1u);
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// naive kernel: one thread per owner, plain sweep loop (GPU restatement of _naive_py,
-// core.py:195-205); independent second implementation used for cross-checks.
-// ------------------------------------------------------------------------------------
-template <typename T, bool STRICT, bool REFL>
-__global__ void rs_naive_kernel(T* __restrict__ A, long long os, long long cs, long long owners, int len,
-                                const T* __restrict__ C, const T* __restrict__ Sm, long long ldcs, int k, int rev) {
-  const long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (o >= owners) return;
-  T* a = A + o * os;
-  for (int p = 0; p < k; ++p) {
-    for (int jj = 0; jj < len - 1; ++jj) {
-      const long long j = rev ? (long long)len - 2 - jj : jj;
-      const T c = C[j + (long long)p * ldcs];
-      const T s = Sm[j + (long long)p * ldcs];
-      T x = a[j * cs];
-      T y = a[(j + 1) * cs];
-      if constexpr (REFL) {
-        const T d = sub_rn(c, s);
-        const T e = add_rn(c, s);
-        refl2<T, STRICT>(x, y, s, d, e);
-      } else {
-        rot2<T, STRICT>(x, y, c, s);
-      }
-      a[j * cs] = x;
-      a[(j + 1) * cs] = y;
-    }
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// FMA-pipe peak probe (roofline denominator: MEASURED_PEAKS.json has no FP64/FP32 entry)
-// ------------------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(256) rs_fma_peak_kernel(T* out, int iters, T a, T b) {
-  T acc[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) acc[c] = (T)(threadIdx.x + c);
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[c] = fma_rn(acc[c], a, b);
-  }
-  T s = 0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s += acc[c];
-  if (s == (T)-1.2345) out[0] = s;
 }
 
 // ------------------------------------------------------------------------------------
@@ -1138,21 +271,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.nchunk = g.nchunk;
   P.nblk = g.nblk;
   P.nw = lp.nw;
-  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL>;
-  {
-    // opt in to the large dynamic shared memory once per (kernel, device)
-    static std::atomic<int> configured{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const int bit = 1 << (dev & 31);
-    if (!(configured.load(std::memory_order_relaxed) & bit)) {
-      int optin = 0;
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-      if (e != cudaSuccess) return fail(RS_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-      configured.fetch_or(bit, std::memory_order_relaxed);
-    }
-  }
+  P.trace = g_trace_buf;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)lp.grid);
   cfg.blockDim = dim3((unsigned)(lp.nw * 32));
@@ -1163,7 +282,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, P);
+  e = hs ? launch_pipeline<T, STRICT, REFL, true>(cfg, P) : launch_pipeline<T, STRICT, REFL, false>(cfg, P);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pipeline launch: ") + cudaGetErrorString(e));
   return RS_OK;
@@ -1674,10 +793,7 @@ rs_status rs_debug_set_trace(void* device_ptr) {
   (void)device_ptr;
   return fail(RS_EUNSUPPORTED, "library built without -DRS_TRACE");
 #endif
-  unsigned long long* p = reinterpret_cast<unsigned long long*>(device_ptr);
-  (void)kTraceWords;
-  cudaError_t e = cudaMemcpyToSymbol(g_trace, &p, sizeof(p));
-  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("rs_debug_set_trace: ") + cudaGetErrorString(e));
+  g_trace_buf = reinterpret_cast<unsigned long long*>(device_ptr);
   return RS_OK;
 }
 
