@@ -168,8 +168,12 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   }
   long long U = mode == 1 ? 4 * grid * q : umin;
   if (U > g.pairs) U = g.pairs;  // at least one sweep per unit
+  // the fewest rounds of <= cap warps, spread evenly (equal rounds keep every round's
+  // warps per sub-partition, and so its latency hiding, the same)
   const long long nmax = (U + grid - 1) / grid;
-  int nw = (int)(((nmax + 3) / 4) * 4);
+  const long long rounds = (nmax + cap - 1) / cap;
+  const long long per_round = (nmax + rounds - 1) / rounds;
+  int nw = (int)(((per_round + 3) / 4) * 4);
   if (nw > cap) nw = cap;
   lp->grid = (int)grid;
   lp->nw = nw;

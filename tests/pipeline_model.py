@@ -62,7 +62,8 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
     U = 4 * G * q if mode == 1 else umin
     U = min(U, g.tiles * g.k)
     nmax = -(-U // G)
-    nw = min(cap, -(-nmax // 4) * 4)
+    rounds = -(-nmax // cap)
+    nw = min(cap, -(-(-(-nmax // rounds)) // 4) * 4)
     return dict(G=G, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw)
 
 

@@ -6,20 +6,23 @@ sys.path.insert(0, os.path.dirname(HERE))
 import numpy as np, torch
 from paper_2412_01852_b200 import apply_device, _lib, flops_applied
 m, n, k = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (4096, 4096, 192)
+side = sys.argv[4] if len(sys.argv) > 4 else "right"
+order = sys.argv[5] if len(sys.argv) > 5 else "forward"
+ln = m if side == "left" else n
 lib = _lib.load()
-info = _lib.plan_info(m, n, k)
+info = _lib.plan_info(m, n, k, side=1 if side == "left" else 0)
 G, NW = info["grid_ctas"], info["warps_per_cta"]
 W, RND = 10, 32
 buf = torch.zeros(G * 16 * RND * W, dtype=torch.int64, device="cuda")
 _lib.check(lib.rs_debug_set_trace(buf.data_ptr()), "trace")
 A = torch.randn(n, m, dtype=torch.float64, device="cuda").t()
-th = torch.rand(k, n - 1, dtype=torch.float64, device="cuda").t() * 6.283185307179586
+th = torch.rand(k, ln - 1, dtype=torch.float64, device="cuda").t() * 6.283185307179586
 C, S = torch.cos(th), torch.sin(th)
 for _ in range(2):
-    buf.zero_(); apply_device(A, (C, S), fast=True)
+    buf.zero_(); apply_device(A, (C, S), fast=True, side=side, order=order)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-buf.zero_(); e0.record(); apply_device(A, (C, S), fast=True); e1.record(); torch.cuda.synchronize()
+buf.zero_(); e0.record(); apply_device(A, (C, S), fast=True, side=side, order=order); e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 rec = buf.cpu().numpy().reshape(G, 16, RND, W)
 valid = rec[..., 1] != 0
@@ -39,7 +42,7 @@ for sv, nm in ((0, "ring"), (1, "global"), (2, "flag")):
     if sel.any():
         t = r[sel, 3:9].sum(axis=0).astype(float)
         print(f"  src={nm:6s} n={sel.sum():5d}:", ", ".join(f"{a} {100*v/t.sum():.1f}%" for a, v in zip(names, t)))
-nblk = (n + 8) // 9 + 1
+nblk = (ln + 8) // 9 + 1
 kbs = (r[:, 9] >> 32) & 0xff
 per_block_compute = r[:, 7].sum() / (len(r) * nblk)
 print("unit widths:", dict(zip(*np.unique(kbs, return_counts=True))))
