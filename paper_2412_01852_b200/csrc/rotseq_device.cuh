@@ -265,6 +265,7 @@ struct PipeParams {
   uint32_t* flags;   // [tiles*k + 1] progress flags of in-place hand-offs, index tile*k + p0
   void* trash;       // 32*R elements: write/read target of lanes past the last row
   int ua;            // units per tile (base)
+  int rev_slots;     // 1: round slot = NW-1-warp (see pipeline_units)
   int len;           // length of the rotated dimension (n right, m left)
   int k;             // sweeps
   int nchunk;        // ceil(len / (K+1))
@@ -447,11 +448,16 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   uint64_t* const full_in = bar_in;
   uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
   uint64_t* const cbar = bar_in + S + 1;
-  // the next position in the same round runs on warp + 1
-  uint64_t* const full_out = bars + (warp + 1) * NBAR;
+  // Round slot of this warp: position p runs on slot p % NW. With rev_slots the slot order
+  // is reversed (slot = NW-1-warp), so chain-downstream units run on older warps, which the
+  // warp scheduler favours; the next position of a round runs on warp + dir.
+  const int dir = P.rev_slots ? -1 : 1;
+  const int slot = P.rev_slots ? NW - 1 - warp : warp;
+  const int wnext = warp + dir;
+  uint64_t* const full_out = bars + (wnext < 0 ? NW : wnext) * NBAR;
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
-  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(wnext < 0 ? NW : wnext) * S * CHUNK;
   unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
 
   const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
@@ -459,7 +465,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
 
   for (int jr = 0;; ++jr) {
-    const long long pos = (long long)jr * NW + warp;
+    const long long pos = (long long)jr * NW + slot;
     if (pos >= npos) break;
     const long long g = pos_to_unit(cr, pos);
     const Unit un = unit_at(g, P.t1, P.ua, k);
@@ -471,11 +477,11 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     int src = SRC_GLOBAL, dst = DST_GLOBAL;
     if (p0 > 0) {
       src = SRC_FLAG;
-      if (warp > 0 && g - 1 >= cr.g0 && unit_to_pos(cr, g - 1) == pos - 1) src = SRC_RING;
+      if (slot > 0 && g - 1 >= cr.g0 && unit_to_pos(cr, g - 1) == pos - 1) src = SRC_RING;
     }
     if (p0 + Kb < k) {
       dst = DST_FLAG;
-      if (warp < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
+      if (slot < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
     }
     const bool self = src != SRC_RING;
 
