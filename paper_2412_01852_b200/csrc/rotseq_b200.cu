@@ -490,14 +490,16 @@ cudaError_t copy_wave_chunk(T* dev, T* host, const Geometry& g, int64_t m, int64
   return copy2d(hptr, (size_t)lda * sizeof(T), dptr, (size_t)m * sizeof(T), width, height, kind, st);
 }
 
+constexpr int kMaxHostChunks = 64;
+constexpr int kCopyLanes = 2;  // streams per direction (copies of a lane run on their own engine)
 struct HostCtx {
   int dev = -1;
-  cudaStream_t cin = nullptr, cout = nullptr;
-  cudaEvent_t e0 = nullptr, ecs = nullptr, eend = nullptr;
+  cudaStream_t cin[kCopyLanes] = {}, cout[kCopyLanes] = {};
+  cudaEvent_t e0 = nullptr, ecs = nullptr, eend[kCopyLanes] = {};
+  cudaEvent_t ein[kMaxHostChunks] = {};  // group i's arrival count is written
   uint32_t* ctl = nullptr;  // arrival / release counters (cudaMalloc: stream memory ops
                             // reject stream-ordered pool addresses)
 };
-constexpr int kMaxHostChunks = 64;
 
 template <typename T>
 rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs, int64_t k,
@@ -518,13 +520,16 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   cudaGetDevice(&dev);
   static thread_local HostCtx ctx;
   if (ctx.dev != dev) {
-    if (cudaStreamCreateWithFlags(&ctx.cin, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx.cout, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx.e0, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx.ecs, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx.eend, cudaEventDisableTiming) != cudaSuccess ||
-        cudaMalloc(reinterpret_cast<void**>(&ctx.ctl), (kMaxHostChunks + 1) * sizeof(uint32_t)) != cudaSuccess)
-      return fail(RS_ECUDA, "stream/event/counter creation failed");
+    bool okc = cudaEventCreateWithFlags(&ctx.e0, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&ctx.ecs, cudaEventDisableTiming) == cudaSuccess &&
+               cudaMalloc(reinterpret_cast<void**>(&ctx.ctl), (kMaxHostChunks + 1) * sizeof(uint32_t)) == cudaSuccess;
+    for (int l = 0; l < kCopyLanes && okc; ++l)
+      okc = cudaStreamCreateWithFlags(&ctx.cin[l], cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&ctx.cout[l], cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx.eend[l], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < kMaxHostChunks && okc; ++i)
+      okc = cudaEventCreateWithFlags(&ctx.ein[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!okc) return fail(RS_ECUDA, "stream/event/counter creation failed");
     ctx.dev = dev;
     // keep stream-ordered allocations cached between calls
     cudaMemPool_t pool;
@@ -534,14 +539,46 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
     }
   }
   // wave-column chunks: ~32 per call, at least 64 columns each
-  int nchunks_target = 8;
+  // Fine chunks (kernel-side arrival/release granularity) copied in groups that ramp up
+  // and down (1, 1, 2, 4, G, ..., G, 4, 2, 1, 1 fine chunks): a small first group lets
+  // the kernel start early, a small last group keeps the copy-out tail short, and the
+  // large middle groups keep the copy engines at full speed.
+  int nchunks_target = 32;
   if (const char* ev = getenv("RS_HOST_CHUNKS")) {
     const int v = atoi(ev);
     if (v >= 1 && v <= kMaxHostChunks) nchunks_target = v;
   }
+  int gmax = 4;
+  if (const char* ev = getenv("RS_HOST_GROUP")) {
+    const int v = atoi(ev);
+    if (v >= 1) gmax = v;
+  }
   int cw = (int)((g.len + nchunks_target - 1) / nchunks_target);
-  if (cw < 64) cw = 64;
+  if (cw < 16) cw = 16;
   const int ncw = (int)((g.len + cw - 1) / cw);
+  int gb[kMaxHostChunks + 1];
+  int ngroups = 0;
+  {
+    static const int ramp[] = {1, 1, 2, 4};
+    int head[8], nh = 0, tailv[8], nt = 0, left = ncw;
+    for (int r : ramp) {
+      const int s = r < gmax ? r : gmax;
+      if (left >= 2 * s) {
+        head[nh++] = s;
+        tailv[nt++] = s;
+        left -= 2 * s;
+      }
+    }
+    gb[0] = 0;
+    int pos = 0;
+    for (int i = 0; i < nh; ++i) gb[++ngroups] = (pos += head[i]);
+    while (left > 0) {
+      const int s = left < gmax ? left : gmax;
+      gb[++ngroups] = (pos += s);
+      left -= s;
+    }
+    for (int i = nt - 1; i >= 0; --i) gb[++ngroups] = (pos += tailv[i]);
+  }
   const size_t abytes = (size_t)m * n * sizeof(T);
   const size_t csbytes = (size_t)(g.len - 1) * k * sizeof(T);
   const size_t wsbytes = g.coef_bytes + g.flag_bytes;
@@ -584,26 +621,39 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   ck(cudaMemsetAsync(ctl, 0, ctlbytes, st), "memset");
   ck(cudaEventRecord(ctx.e0, st), "event");
   // copy-in stream: C, S, then A chunk by chunk, each followed by its arrival count
-  ck(cudaStreamWaitEvent(ctx.cin, ctx.e0, 0), "wait");
+  int lanes = kCopyLanes;
+  if (const char* ev = getenv("RS_HOST_LANES")) {
+    const int v = atoi(ev);
+    if (v >= 1 && v <= kCopyLanes) lanes = v;
+  }
+  for (int l = 0; l < lanes; ++l) ck(cudaStreamWaitEvent(ctx.cin[l], ctx.e0, 0), "wait");
   const size_t lc = (size_t)(g.len - 1);
   ck(copy2d(dC, lc * sizeof(T), C, (size_t)ldcs * sizeof(T), lc * sizeof(T), (size_t)k, cudaMemcpyHostToDevice,
-            ctx.cin), "C copy");
+            ctx.cin[0]), "C copy");
   ck(copy2d(dS, lc * sizeof(T), S, (size_t)ldcs * sizeof(T), lc * sizeof(T), (size_t)k, cudaMemcpyHostToDevice,
-            ctx.cin), "S copy");
-  ck(cudaEventRecord(ctx.ecs, ctx.cin), "event");
-  mark(ctx.cin, "cs_in");
-  for (int i = 0; i < ncw && e == cudaSuccess; ++i) {
-    if (i == ncw - 1) mark(ctx.cin, "a_in_last_start");
-    const long long v0 = (long long)i * cw, v1 = v0 + cw < g.len ? v0 + cw : g.len;
-    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyHostToDevice, ctx.cin), "A copy-in");
-    const CUresult r = ops.write(reinterpret_cast<CUstream>(ctx.cin), reinterpret_cast<CUdeviceptr>(ctl),
-                                 (cuuint32_t)(i + 1), 0);
+            ctx.cin[0]), "S copy");
+  ck(cudaEventRecord(ctx.ecs, ctx.cin[0]), "event");
+  mark(ctx.cin[0], "cs_in");
+  static const char* kInNames[] = {"in0", "in1", "in2", "in3", "in4", "in5", "in6", "in7", "in8", "in9"};
+  static const char* kOutNames[] = {"out0", "out1", "out2", "out3", "out4", "out5", "out6", "out7", "out8", "out9"};
+  // groups alternate over the copy lanes; a group's arrival count is written only after
+  // the previous group's (event chain), so the counter only grows
+  for (int gi = 0; gi < ngroups && e == cudaSuccess; ++gi) {
+    cudaStream_t cs_ = ctx.cin[gi % lanes];
+    if (gi < 10) mark(cs_, kInNames[gi]);
+    const long long v0 = (long long)gb[gi] * cw;
+    const long long v1 = (long long)gb[gi + 1] * cw < g.len ? (long long)gb[gi + 1] * cw : g.len;
+    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyHostToDevice, cs_), "A copy-in");
+    if (gi > 0 && lanes > 1) ck(cudaStreamWaitEvent(cs_, ctx.ein[gi - 1], 0), "wait");
+    const CUresult r = ops.write(reinterpret_cast<CUstream>(cs_), reinterpret_cast<CUdeviceptr>(ctl),
+                                 (cuuint32_t)gb[gi + 1], 0);
+    ck(cudaEventRecord(ctx.ein[gi], cs_), "event");
     if (r != CUDA_SUCCESS) {
       ck(cudaErrorUnknown, "cuStreamWriteValue32");
       g_err += " (CUresult " + std::to_string((int)r) + ")";
     }
   }
-  mark(ctx.cin, "a_in_done");
+  mark(ctx.cin[(ngroups - 1) % lanes], "a_in_done");
   // compute stream: pack once C/S are in, then the streaming pipeline kernel
   ck(cudaStreamWaitEvent(st, ctx.ecs, 0), "wait");
   mark(st, "pack_start");
@@ -616,21 +666,27 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
     mark(st, "kernel_end");
   }
   // copy-out stream: chunk i leaves once every tile's final unit has released it
-  ck(cudaStreamWaitEvent(ctx.cout, ctx.e0, 0), "wait");
-  for (int i = 0; i < ncw && e == cudaSuccess && rc == RS_OK; ++i) {
-    const CUresult r = ops.wait(reinterpret_cast<CUstream>(ctx.cout), reinterpret_cast<CUdeviceptr>(ctl + 1 + i),
-                                (cuuint32_t)g.tiles, CU_STREAM_WAIT_VALUE_GEQ);
+  for (int l = 0; l < lanes; ++l) ck(cudaStreamWaitEvent(ctx.cout[l], ctx.e0, 0), "wait");
+  for (int gi = 0; gi < ngroups && e == cudaSuccess && rc == RS_OK; ++gi) {
+    // final units release chunks in order, so the group's last chunk implies the rest
+    cudaStream_t co_ = ctx.cout[gi % lanes];
+    const CUresult r = ops.wait(reinterpret_cast<CUstream>(co_),
+                                reinterpret_cast<CUdeviceptr>(ctl + gb[gi + 1]), (cuuint32_t)g.tiles,
+                                CU_STREAM_WAIT_VALUE_GEQ);
     if (r != CUDA_SUCCESS) {
       ck(cudaErrorUnknown, "cuStreamWaitValue32");
       g_err += " (CUresult " + std::to_string((int)r) + ")";
     }
-    const long long v0 = (long long)i * cw, v1 = v0 + cw < g.len ? v0 + cw : g.len;
-    if (i == 0 || i == ncw - 1) mark(ctx.cout, i == 0 ? "out_first_start" : "out_last_start");
-    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyDeviceToHost, ctx.cout), "A copy-out");
+    const long long v0 = (long long)gb[gi] * cw;
+    const long long v1 = (long long)gb[gi + 1] * cw < g.len ? (long long)gb[gi + 1] * cw : g.len;
+    if (gi < 10) mark(co_, kOutNames[gi]);
+    ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyDeviceToHost, co_), "A copy-out");
   }
-  mark(ctx.cout, "out_done");
-  ck(cudaEventRecord(ctx.eend, ctx.cout), "event");
-  ck(cudaStreamWaitEvent(st, ctx.eend, 0), "wait");
+  mark(ctx.cout[(ngroups - 1) % lanes], "out_done");
+  for (int l = 0; l < lanes; ++l) {
+    ck(cudaEventRecord(ctx.eend[l], ctx.cout[l]), "event");
+    ck(cudaStreamWaitEvent(st, ctx.eend[l], 0), "wait");
+  }
   cudaFreeAsync(mem, st);
   cudaError_t es = cudaStreamSynchronize(st);
   if (dbg) {
