@@ -255,8 +255,6 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.units = lp.units;
   P.t1 = lp.t1;
   P.ua = lp.ua;
-  P.rev_slots = 0;
-  if (const char* ev = getenv("RS_REV_SLOTS")) P.rev_slots = atoi(ev) != 0;
   P.coef = coef;
   P.flags = flags;
   P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only + 256;

@@ -265,7 +265,6 @@ struct PipeParams {
   uint32_t* flags;   // [tiles*k + 1] progress flags of in-place hand-offs, index tile*k + p0
   void* trash;       // 32*R elements: write/read target of lanes past the last row
   int ua;            // units per tile (base)
-  int rev_slots;     // 1: round slot = NW-1-warp (see pipeline_units)
   int len;           // length of the rotated dimension (n right, m left)
   int k;             // sweeps
   int nchunk;        // ceil(len / (K+1))
@@ -448,16 +447,12 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   uint64_t* const full_in = bar_in;
   uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
   uint64_t* const cbar = bar_in + S + 1;
-  // Round slot of this warp: position p runs on slot p % NW. With rev_slots the slot order
-  // is reversed (slot = NW-1-warp), so chain-downstream units run on older warps, which the
-  // warp scheduler favours; the next position of a round runs on warp + dir.
-  const int dir = P.rev_slots ? -1 : 1;
-  const int slot = P.rev_slots ? NW - 1 - warp : warp;
-  const int wnext = warp + dir;
-  uint64_t* const full_out = bars + (wnext < 0 ? NW : wnext) * NBAR;
+  // position p of a round runs on warp p % NW; the next position on warp + 1
+  const int slot = warp;
+  uint64_t* const full_out = bars + (warp + 1) * NBAR;
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
-  T* const rout = ring_sm + (size_t)(wnext < 0 ? NW : wnext) * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
   unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
 
   const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);

@@ -57,3 +57,11 @@ def both_halves():
     with torch.cuda.stream(s1): dAf[:half].copy_(hAf[:half], non_blocking=True)
     with torch.cuda.stream(s2): hAf[half:].copy_(dBf[half:], non_blocking=True)
 print("H2D(1st half)||D2H(2nd half) same buffer %.3f ms" % t(both_halves))
+def both_chunked(nc=32):
+    step = m * n // nc
+    for i in range(nc):
+        with torch.cuda.stream(s1): dAf[i*step:(i+1)*step].copy_(hAf[i*step:(i+1)*step], non_blocking=True)
+        with torch.cuda.stream(s2): hBf[i*step:(i+1)*step].copy_(dBf[i*step:(i+1)*step], non_blocking=True)
+hBf = torch.as_strided(hB, (m * n,), (1,))
+for nc in (8, 32, 64):
+    print("H2D||D2H chunked %d: %.3f ms" % (nc, t(lambda: both_chunked(nc))))
