@@ -1,7 +1,7 @@
 // pipeline_variant.cu — one pipeline-kernel family per compilation: build.py compiles
 // this file once per (RS_VARIANT_T, RS_VARIANT_STRICT, RS_VARIANT_REFL) so the eight
-// fully unrolled kernel families (each with its resident and host-streaming variant)
-// build in parallel. The launcher opts the kernel in to the device's full dynamic shared
+// fully unrolled kernel families (each with its resident / host-streaming and right /
+// left-side variants) build in parallel. The launcher opts the kernel in to the device's full dynamic shared
 // memory once per device and launches it (cooperative: all CTAs co-resident).
 #include "rotseq_device.cuh"
 
@@ -11,9 +11,9 @@
 
 namespace rsk {
 
-template <typename T, bool STRICT, bool REFL, bool HS>
+template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) {
-  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL, HS>;
+  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL, HS, LEFT>;
   static std::atomic<int> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -28,9 +28,12 @@ cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) 
   return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
-template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, false>(
-    const cudaLaunchConfig_t&, const PipeParams&);
-template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, true>(
-    const cudaLaunchConfig_t&, const PipeParams&);
+#define RS_INST(HS, LEFT)                                                                                 \
+  template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, HS, LEFT>( \
+      const cudaLaunchConfig_t&, const PipeParams&);
+RS_INST(false, false)
+RS_INST(true, false)
+RS_INST(false, true)
+RS_INST(true, true)
 
 }  // namespace rsk

@@ -286,7 +286,12 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = hs ? launch_pipeline<T, STRICT, REFL, true>(cfg, P) : launch_pipeline<T, STRICT, REFL, false>(cfg, P);
+  const bool left = g.os != 1;  // owners are columns: owner-major rings, coalesced A I/O
+  if (hs)
+    e = left ? launch_pipeline<T, STRICT, REFL, true, true>(cfg, P) : launch_pipeline<T, STRICT, REFL, true, false>(cfg, P);
+  else
+    e = left ? launch_pipeline<T, STRICT, REFL, false, true>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false>(cfg, P);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pipeline launch: ") + cudaGetErrorString(e));
   return RS_OK;

@@ -353,10 +353,10 @@ __host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, lon
 //   or to A (global) through one generic store path, so a unit width compiles to ONE loop
 //   body (instruction-cache footprint). EDGE blocks check every column and lane at run time.
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED>
+template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT>
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
-                                          const T* __restrict__ islot, T* const (&op)[R], const long long (&ostr)[R],
+                                          const T* islot, T* const (&op)[R], const long long (&ostr)[R],
                                           int b, int len, int Kb, int lane, bool has_in_rt, bool has_out_rt) {
   constexpr int TR = 32 * R;
   constexpr int NL = EDGE ? K : KB;
@@ -370,6 +370,20 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   for (int r = 0; r < R; ++r) q[r] = op[r];
 #pragma unroll
   for (int u = 0; u <= K; ++u) {
+    // incoming column (LEFT rings are owner-major [owner][K+1]; right rings wave-major)
+    T nv[R];
+    {
+      const long long col = c0 + u;
+      if (!EDGE || (has_in && col < len)) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          nv[r] = islot[LEFT ? (lane + 32 * r) * (K + 1) + u : u * TR + lane + 32 * r];
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) nv[r] = T(0);
+      }
+    }
+    // outgoing column (LEFT may stage it in place of the column just read)
     if (has_out) {
       const long long col = c0 - (K + 1) + u;
       if (!EDGE || col < len) {
@@ -385,16 +399,8 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
 #pragma unroll
       for (int r = 0; r < R; ++r) q[r] += ostr[r];
     }
-    {
-      const long long col = c0 + u;
-      if (!EDGE || (has_in && col < len)) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) w[r][u] = islot[u * TR + lane + 32 * r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) w[r][u] = T(0);
-      }
-    }
+    for (int r = 0; r < R; ++r) w[r][u] = nv[r];
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       constexpr int M = K + 1;
@@ -420,7 +426,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
 // ------------------------------------------------------------------------------------
 // the persistent pipeline kernel
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED, bool HS>
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED, bool HS, bool LEFT>
 __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned char* smem_raw) {
   using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
   constexpr int TR = 32 * R;
@@ -489,6 +495,14 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
       gcs[r] = ok ? P.cs : 0;
     }
+    // LEFT coalesced chunk copies: this lane's first element e = lane is owner lo0, column
+    // lv0; each step of 32 elements advances 3 owners + 5 columns (wrapping past K+1)
+    static_assert(32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
+    const int lo0 = lane / (K + 1), lv0 = lane - lo0 * (K + 1);
+    const long long lstep = 3 * P.os + (32 - 3 * (K + 1)) * P.cs;
+    const long long lwrap = P.os - (K + 1) * P.cs;
+    const T* const lbase = A + (tile * TR + lo0) * P.os + lv0 * P.cs;
+    const bool lfull = tile * TR + TR <= P.owners;
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
     // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
     const int part = tile < P.t1 ? 1 : 0;
@@ -532,6 +546,36 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       }
       T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
       const long long c0 = (long long)q * (K + 1);
+      if constexpr (LEFT) {
+        // owner-major chunk [TR owners][K+1 columns]: element e = i*32 + lane is owner
+        // e/(K+1), column e%(K+1) — consecutive lanes read consecutive columns of one owner
+        // (contiguous in A on the left side) and write consecutive shared words. (owner,
+        // column) and the address advance incrementally (e += 32: +3 owners, +5 columns).
+        int v = lv0;
+        const T* sp = lbase + c0 * P.cs;
+        if (lfull && c0 + K < len) {
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            cp_async_elem(dstp + i * 32 + lane, sp, true);
+            v += 32 - 3 * (K + 1);
+            sp += lstep;
+            if (v >= K + 1) v -= K + 1, sp += lwrap;
+          }
+        } else {
+          int ol = lo0;
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            const bool ok = tile * TR + ol < P.owners && c0 + v < len;
+            cp_async_elem(dstp + i * 32 + lane, ok ? sp : A, ok);
+            v += 32 - 3 * (K + 1);
+            ol += 3;
+            sp += lstep;
+            if (v >= K + 1) v -= K + 1, ++ol, sp += lwrap;
+          }
+        }
+        cp_async_commit();
+        return;
+      }
       const T* sp[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) sp[r] = grow[r] + c0 * gcs[r];
@@ -597,7 +641,17 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       // output pointers: the consumer's ring slot (column stride TR) or A (stride gcs)
       T* op[R];
       long long ostr[R];
-      if (outring) {
+      // LEFT, output to A: stage the outgoing chunk in the input slot just read (the last
+      // block, which has no input, reuses the previous block's slot) and copy it out below
+      T* stage = const_cast<T*>(b < nchunk ? islot : rin + ((iseq - 1u) % S) * CHUNK);
+      if (LEFT && outring) {
+        T* oslot = rout + (oseq % S) * CHUNK;
+#pragma unroll
+        for (int r = 0; r < R; ++r) op[r] = oslot + (lane + 32 * r) * (K + 1), ostr[r] = 1;
+      } else if (LEFT) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) op[r] = stage + (lane + 32 * r) * (K + 1), ostr[r] = 1;
+      } else if (outring) {
         T* oslot = rout + (oseq % S) * CHUNK + lane;
 #pragma unroll
         for (int r = 0; r < R; ++r) op[r] = oslot + 32 * r, ostr[r] = TR;
@@ -613,13 +667,45 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       // ring credit: the producer runs at most `credit` chunks ahead of its consumer
       if (outring && has_out && oseq >= credit) wait_count(consumed_out, oseq - credit + 1u);
       unsigned long long t4 = trace_clock();
-      run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED>(
+      run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT>(
           w, reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF), islot, op, ostr, b, len, Kb, lane, b < nchunk,
           b >= 1);
       __syncwarp();
+      if (LEFT && !outring && has_out) {  // copy the staged chunk to A, columns contiguous
+        const long long cb0 = (long long)(b - 1) * (K + 1);
+        int v = lv0;
+        T* dp = const_cast<T*>(lbase) + cb0 * P.cs;
+        if (lfull && cb0 + K < len) {
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            *dp = stage[i * 32 + lane];
+            v += 32 - 3 * (K + 1);
+            dp += lstep;
+            if (v >= K + 1) v -= K + 1, dp += lwrap;
+          }
+        } else {
+          int ol = lo0;
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            if (tile * TR + ol < P.owners && cb0 + v < len) *dp = stage[i * 32 + lane];
+            v += 32 - 3 * (K + 1);
+            ol += 3;
+            dp += lstep;
+            if (v >= K + 1) v -= K + 1, ++ol, dp += lwrap;
+          }
+        }
+        __syncwarp();
+      }
       unsigned long long t5 = trace_clock();
       if (lane == 0) {
-        if (has_in) st_release_shared(consumed_in, iseq + 1u);
+        // LEFT global output: the last block stages in the slot of chunk nchunk-1, so that
+        // slot is released one block later (as nchunk, i.e. iseq of the last block)
+        if (LEFT && !outring) {
+          if (has_in && b + 1 < nchunk) st_release_shared(consumed_in, iseq + 1u);
+          if (b == nchunk) st_release_shared(consumed_in, iseq);
+        } else if (has_in) {
+          st_release_shared(consumed_in, iseq + 1u);
+        }
         if (outring && has_out) mbar_arrive(&full_out[oseq % S]);
         if (dst == DST_FLAG && has_out && (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
           // the warp barrier above orders every lane's stores before lane 0's gpu-scope
@@ -677,7 +763,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 
 // HS: host-streaming variant (rs_apply_host_*), a separate instantiation so the resident
 // path carries none of its checks
-template <typename T, int K, int R, bool STRICT, bool REFL, bool HS>
+template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
   constexpr int S = kStages;
   constexpr int NBAR = kCtlWords;
@@ -700,11 +786,11 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __
   // fast mode: the scaled form, unless the pack found coefficients outside its safe range
   if constexpr (!STRICT) {
     if (P.use_scaled && *P.unsafe == 0u) {
-      pipeline_units<T, K, R, STRICT, REFL, true, HS>(P, smem_raw);
+      pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
       return;
     }
   }
-  pipeline_units<T, K, R, STRICT, REFL, false, HS>(P, smem_raw);
+  pipeline_units<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
 }
 
 // ------------------------------------------------------------------------------------
@@ -894,7 +980,7 @@ __global__ void __launch_bounds__(256) rs_fma_peak_kernel(T* out, int iters, T a
 
 // Launches the pipeline kernel family <T, STRICT, REFL, HS> (defined and explicitly
 // instantiated in pipeline_variant.cu, one translation unit per family).
-template <typename T, bool STRICT, bool REFL, bool HS>
+template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P);
 
 }  // namespace rsk

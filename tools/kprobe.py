@@ -32,6 +32,8 @@ print(os.environ.get("TAG", ""), " | ".join(out), flush=True)
 CASES = [(4096, 4096, 192, "f64", "right", "forward"), (65536, 2048, 256, "f64", "right", "forward"),
          (8192, 8192, 128, "f32", "right", "forward"), (16384, 16384, 96, "f64", "left", "reverse"),
          (8192, 2048, 256, "f64", "right", "forward")]
+if os.environ.get("KP_CASES"):
+    CASES = json.loads(os.environ["KP_CASES"])
 for tag in (sys.argv[1:] or ["default"]):
     env = dict(os.environ, CASES=json.dumps(CASES), TAG=tag)
     for kv in tag.split(","):
