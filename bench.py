@@ -308,6 +308,7 @@ def main():
         flush.zero_()
     torch.cuda.synchronize(dev)
     sampler.active = False
+    sampler.stop()  # the nvidia-smi poller perturbs launch-heavy host code (e2e below)
     launches = _lib.launch_count() - launches0
     if world > 1:
         dist.barrier()
@@ -392,7 +393,6 @@ def main():
             cpu_baseline = {"value": None, "unit": "GFLOP/s", "cores": cpu_threads(), "kind": "port",
                             "sample": f"failed: {exc}"}
 
-    sampler.stop()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": n_gpus, "steps": args.steps,

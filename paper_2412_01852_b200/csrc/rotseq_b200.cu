@@ -551,7 +551,7 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
     const int v = atoi(ev);
     if (v >= 1 && v <= kMaxHostChunks) nchunks_target = v;
   }
-  int gmax = 4;
+  int gmax = 4;  // groups of 4 fine chunks (~17 MB at config 2) keep the copy engines efficient
   if (const char* ev = getenv("RS_HOST_GROUP")) {
     const int v = atoi(ev);
     if (v >= 1) gmax = v;

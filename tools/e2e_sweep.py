@@ -10,7 +10,7 @@ hC = torch.from_numpy(np.asfortranarray(np.cos(th))).pin_memory()
 hS = torch.from_numpy(np.asfortranarray(np.sin(th))).pin_memory()
 configs = [c.split(":") for c in (sys.argv[1:] or ["8:1", "8:8", "16:4", "64:4", "64:8"])]
 res = {tuple(c): [] for c in configs}
-for rep in range(4):
+for rep in range(int(os.environ.get('REPS', '4'))):
     for c in configs:
         os.environ["RS_HOST_CHUNKS"], os.environ["RS_HOST_GROUP"] = c
         apply_host(hA, (hC, hS), fast=True)
