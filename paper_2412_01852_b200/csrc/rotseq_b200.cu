@@ -81,12 +81,14 @@ struct Geometry {
   size_t coef_bytes = 0;    // standard + scaled records
   size_t flags_only = 0;    // progress flags (zeroed per launch)
   size_t flag_bytes = 0;    // flags + unsafe word + trash slot
+  bool left = false;
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int kind, int dtype, Geometry* g) {
   const bool left = side == RS_SIDE_LEFT;
+  g->left = left;
   g->owners = left ? n : m;
   g->len = (int)(left ? m : n);
   g->os = left ? lda : 1;
@@ -136,7 +138,8 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   const size_t per = smem_per_warp(tsz, g.coef_rec);
   // one extra control block: the (never dereferenced) out-ring words of the last warp
   int cap = (int)((optin - kCtlWords * sizeof(uint64_t)) / per);
-  if (cap > kMaxWarps) cap = kMaxWarps;
+  const int wmax = g.left ? kMaxWarpsLeft : kMaxWarps;
+  if (cap > wmax) cap = wmax;
   cap &= ~3;
   if (cap < 4) return fail(RS_EUNSUPPORTED, "shared memory too small for one warp per sub-partition");
   long long grid = sms;

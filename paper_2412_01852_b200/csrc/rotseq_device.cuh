@@ -26,11 +26,17 @@ constexpr int kR = 2;          // owners (rows) per thread
 #ifndef RS_FLAG_EVERY
 #define RS_FLAG_EVERY 8
 #endif
+#ifndef RS_FLAG_TAIL
+#define RS_FLAG_TAIL 1  // progress is published every block in the last RS_FLAG_TAIL blocks
+#endif
 #ifndef RS_STAGES
 #define RS_STAGES 2
 #endif
 constexpr int kStages = RS_STAGES;  // ring depth in chunks of K+1 columns (self-fill runs S-1 ahead)
 constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
+// Left side: the owner-major chunk copies need more registers; 12 warps (170 registers per
+// thread) keep the unrolled body free of spills.
+constexpr int kMaxWarpsLeft = 12;
 constexpr int kTileOwners = 32 * kR;
 constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
 constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
@@ -139,7 +145,26 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // The suspend-time hint parks a waiting warp in hardware until the phase completes instead
 // of spinning: spinning waits would steal issue slots from the warps sharing its SM
 // sub-partition (measured: ~14% of all issued instructions without the hint).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+#ifdef RS_X_SLEEP
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(RS_X_SLEEP);
+}
+#else
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifndef RS_X_NOFASTWAIT
+  if (mbar_test(bar, parity)) return;  // already complete: skip try_wait's fixed latency
+#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "RS_WAIT_%=:\n\t"
@@ -148,6 +173,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(kSuspendHintNs)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -187,7 +213,11 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
+#ifdef RS_X_RELAXED_CONSUMED
+  asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+#else
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+#endif
 }
 __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
   uint32_t v;
@@ -294,6 +324,27 @@ struct Unit {
   int p0;  // first sweep
   int kb;  // sweeps (1..kK)
 };
+// First sweep of unit i (of ut) of a tile: the k sweeps split evenly, except that with
+// RS_X_HEAD=h (percent) the chain's head unit (i = 0) gets h% of the average width.
+__host__ __device__ __forceinline__ int sweep_start(long long i, int ut, int k) {
+#ifdef RS_X_HEAD
+  if (ut > 1) {
+    int hw = (int)((long long)k * RS_X_HEAD / (100LL * ut));
+    if (hw < 1) hw = 1;
+    if ((long long)(k - hw) > (long long)(ut - 1) * kK) return (int)(i * k / ut);
+    if (i == 0) return 0;
+    return hw + (int)((i - 1) * (k - hw) / (ut - 1));
+  }
+#endif
+#ifdef RS_X_TAPER
+  // widths taper linearly along the chain: head (1 + a) x average, tail (1 - a) x average
+  if (ut > 1 && (double)k / ut * (1.0 + fabs(RS_X_TAPER / 100.0)) <= kK - 0.5) {
+    const double x = (double)i / ut, a = RS_X_TAPER / 100.0;
+    return (int)floor(k * (x + a * x * (1.0 - x)) + 0.5);
+  }
+#endif
+  return (int)(i * k / ut);
+}
 __host__ __device__ __forceinline__ long long tile_first_unit(long long t, long long t1, int ua) {
   return t < t1 ? t * (ua + 1) : t1 * (ua + 1) + (t - t1) * ua;
 }
@@ -312,8 +363,8 @@ __host__ __device__ __forceinline__ Unit unit_at(long long g, long long t1, int 
     i = r - (u.tile - t1) * ua;
     ut = ua;
   }
-  u.p0 = (int)(i * k / ut);
-  u.kb = (int)((i + 1) * k / ut) - u.p0;
+  u.p0 = sweep_start(i, ut, k);
+  u.kb = sweep_start(i + 1, ut, k) - u.p0;
   return u;
 }
 // CTA c runs units [g0, g1). When the range ends inside a tile whose first unit lies inside
@@ -353,11 +404,25 @@ __host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, lon
 //   or to A (global) through one generic store path, so a unit width compiles to ONE loop
 //   body (instruction-cache footprint). EDGE blocks check every column and lane at run time.
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT>
+template <typename T>
+__device__ __forceinline__ void st_shared(uint32_t a, T v) {
+  if constexpr (sizeof(T) == 8) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"((double)v) : "memory");
+  } else {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"((float)v) : "memory");
+  }
+}
+// OUTS: the output columns go to shared memory (the next unit's ring, or the left side's
+// staging slot) at obase + u*OSU + r*OSR elements and are stored with STS; otherwise to A
+// through the generic pointers op[r] (stride ostr[r]).
+template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT, bool OUTS>
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* islot, T* const (&op)[R], const long long (&ostr)[R],
-                                          int b, int len, int Kb, int lane, bool has_in_rt, bool has_out_rt) {
+                                          uint32_t obase, int b, int len, int Kb, int lane, bool has_in_rt,
+                                          bool has_out_rt) {
+  constexpr uint32_t OSU = (LEFT ? 1 : 32 * R) * sizeof(T);
+  constexpr uint32_t OSR = (LEFT ? 32 * (K + 1) : 32) * sizeof(T);
   constexpr int TR = 32 * R;
   constexpr int NL = EDGE ? K : KB;
   const long long c0 = (long long)b * (K + 1);
@@ -389,15 +454,22 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
       if (!EDGE || col < len) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if constexpr (SCALED) {
-            *q[r] = mul_rn(w[r][u], sc[u]);
+          const T v = SCALED ? mul_rn(w[r][u], sc[u]) : w[r][u];
+          if constexpr (OUTS) {
+            st_shared<T>(obase + u * OSU + r * OSR, v);
           } else {
-            *q[r] = w[r][u];
+#ifndef RS_X_NOGSTORE
+            *q[r] = v;
+#else
+            if (v == T(1.2345e-300)) *q[r] = v;
+#endif
           }
         }
       }
+      if constexpr (!OUTS) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) q[r] += ostr[r];
+        for (int r = 0; r < R; ++r) q[r] += ostr[r];
+      }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) w[r][u] = nv[r];
@@ -520,7 +592,9 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     auto issue_coef = [&](int b, uint32_t buf) {
       if (lane == 0) {
         uint64_t* bar = &cbar[buf];
+#ifndef RS_X_NOPROXYFENCE
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
         mbar_expect_tx(bar, blk_bytes);
         bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
       }
@@ -537,6 +611,9 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     // progress flag): cp.async (LDGSTS) straight into this warp's own ring, FA chunks ahead.
     uint32_t flag_seen = 0;
     auto fill_chunk = [&](int q) {
+#ifdef RS_X_NOFILL
+      if (src == SRC_GLOBAL) { cp_async_commit(); return; }
+#endif
       if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
       if (HS && src == SRC_GLOBAL) {  // host streaming: wait for the copy of these columns
         long long cend = (long long)q * (K + 1) + K;
@@ -630,7 +707,11 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       constexpr int KB = decltype(kb_c)::value;
       constexpr bool EDGE = decltype(edge_c)::value;
       unsigned long long t0 = trace_clock();
+#ifdef RS_X_NOCOEF
+      if (b + 1 < nblk && b < 1) issue_coef(b + 1, (cseq + 1) & 1);
+#else
       if (b + 1 < nblk) issue_coef(b + 1, (cseq + 1) & 1);
+#endif
       const bool has_in = !EDGE || b < nchunk;
       const bool has_out = !EDGE || b >= 1;
       if (self && b + FA < nchunk) fill_chunk(b + FA);
@@ -660,16 +741,31 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 #pragma unroll
         for (int r = 0; r < R; ++r) op[r] = grow[r] + cb0 * gcs[r], ostr[r] = gcs[r];
       }
+#ifdef RS_X_NOCOEF
+      if (b < 2) mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
+#else
       mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
+#endif
       unsigned long long t2 = trace_clock();
+#ifndef RS_X_NOSYNC
       if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+#endif
       unsigned long long t3 = trace_clock();
       // ring credit: the producer runs at most `credit` chunks ahead of its consumer
+#ifndef RS_X_NOSYNC
       if (outring && has_out && oseq >= credit) wait_count(consumed_out, oseq - credit + 1u);
+#endif
       unsigned long long t4 = trace_clock();
-      run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT>(
-          w, reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF), islot, op, ostr, b, len, Kb, lane, b < nchunk,
-          b >= 1);
+      {
+        const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF);
+        if (LEFT || outring) {
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, smem_u32(op[0]), b,
+                                                                          len, Kb, lane, b < nchunk, b >= 1);
+        } else {
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, 0u, b, len, Kb,
+                                                                           lane, b < nchunk, b >= 1);
+        }
+      }
       __syncwarp();
       if (LEFT && !outring && has_out) {  // copy the staged chunk to A, columns contiguous
         const long long cb0 = (long long)(b - 1) * (K + 1);
@@ -707,7 +803,8 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
           st_release_shared(consumed_in, iseq + 1u);
         }
         if (outring && has_out) mbar_arrive(&full_out[oseq % S]);
-        if (dst == DST_FLAG && has_out && (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b == nblk - 1)) {
+        if (dst == DST_FLAG && has_out &&
+            (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b >= nblk - RS_FLAG_TAIL)) {
           // the warp barrier above orders every lane's stores before lane 0's gpu-scope
           // fence; the release store then publishes "chunks 0..b-1 are in A"
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
@@ -731,7 +828,11 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_in[(iseq + 1u) % S]);
       }
+#ifdef RS_X_NOCOEF
+      if (b < 2) ++cseq;
+#else
       ++cseq;
+#endif
       unsigned long long t6 = trace_clock();
       tacc.c[0] += t1 - t0;
       tacc.c[1] += t2 - t1;
@@ -764,7 +865,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 // HS: host-streaming variant (rs_apply_host_*), a separate instantiation so the resident
 // path carries none of its checks
 template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
+__global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
   constexpr int S = kStages;
   constexpr int NBAR = kCtlWords;
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
@@ -814,10 +915,10 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
     const int ut = ua + part;
     // unit i of this partition holding sweep p: p0(i) = floor(i*k/ut)
     int i = (int)(((long long)p * ut) / k);
-    while (i + 1 < ut && (int)(((long long)(i + 1) * k) / ut) <= p) ++i;
-    while (i > 0 && (int)(((long long)i * k) / ut) > p) --i;
-    const int p0 = (int)(((long long)i * k) / ut);
-    const int kb = (int)(((long long)(i + 1) * k) / ut) - p0;
+    while (i + 1 < ut && sweep_start(i + 1, ut, k) <= p) ++i;
+    while (i > 0 && sweep_start(i, ut, k) > p) --i;
+    const int p0 = sweep_start(i, ut, k);
+    const int kb = sweep_start(i + 1, ut, k) - p0;
     const int l = p - p0;
     Coef<T, REFL>* dst = out + (size_t)part * k * per_p + (size_t)p0 * per_p + l;
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < per_p; x += gridDim.x * blockDim.x) {
@@ -888,8 +989,8 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     const int i = row - part * (ua + 1);  // unit index within the tile
     const int ut = ua + part;
     if (i >= ut) continue;
-    const int p0 = (int)(((long long)i * k) / ut);
-    const int kb = (int)(((long long)(i + 1) * k) / ut) - p0;
+    const int p0 = sweep_start(i, ut, k);
+    const int kb = sweep_start(i + 1, ut, k) - p0;
     const int brec = kb * (K + 1) + kScaleRecs;
     SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
                       (size_t)i * nblk * kScaleRecs;

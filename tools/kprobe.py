@@ -39,4 +39,7 @@ for tag in (sys.argv[1:] or ["default"]):
     for kv in tag.split(","):
         if "=" in kv:
             k, v = kv.split("=", 1); env[k] = v
-    subprocess.run([sys.executable, "-c", code], env=env, timeout=600)
+    try:
+        subprocess.run([sys.executable, "-c", code], env=env, timeout=float(os.environ.get("KP_TIMEOUT", 600)))
+    except subprocess.TimeoutExpired:
+        print(tag, "TIMEOUT", flush=True)

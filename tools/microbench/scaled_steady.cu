@@ -102,6 +102,10 @@ void run(int warps) {
 int main(int argc, char** argv) {
   if (argc > 1 && argv[1][0] == '3') { run<8, 7, 3, true, 0>(12); return 0; }
   if (argc > 1 && argv[1][0] == '2') { run<8, 7, 2, true, 0>(12); return 0; }
-  run<8, 7, 2, true, 0>(12); run<8, 7, 3, true, 0>(12);
+  run<8, 8, 2, true, 0>(8); run<8, 8, 2, true, 0>(12); run<8, 8, 2, true, 0>(16);
+  run<8, 8, 2, true, 1>(12); run<8, 8, 2, true, 2>(12); run<8, 8, 2, true, 3>(12);
+  run<8, 8, 3, true, 0>(8); run<8, 8, 3, true, 0>(12);
+  run<8, 8, 4, true, 0>(8);
+  run<8, 8, 2, false, 0>(12);
   return 0;
 }
