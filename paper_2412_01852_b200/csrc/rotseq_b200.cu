@@ -116,13 +116,14 @@ struct LaunchPlan {
   long long units = 0;
   int ua = 0;
   long long t1 = 0;
+  int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units, several rounds
 };
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec) {
   size_t cbuf = (size_t)(kK + 1) * kK * coef_rec;  // == coef_buf_bytes<T, REFL>()
   const size_t scl = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
   if (scl > cbuf) cbuf = scl;
-  return 2 * cbuf + (size_t)kStages * (kK + 1) * kTileOwners * tsz + kCtlWords * sizeof(uint64_t);
+  return 2 * cbuf + (size_t)stages_for(tsz) * (kK + 1) * kTileOwners * tsz + ctl_words(stages_for(tsz)) * sizeof(uint64_t);
 }
 
 // Grid of G <= #SMs persistent CTAs and U = 4*G*q units (q per SM sub-partition, each
@@ -137,7 +138,8 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
   const size_t per = smem_per_warp(tsz, g.coef_rec);
   // one extra control block: the (never dereferenced) out-ring words of the last warp
-  int cap = (int)((optin - kCtlWords * sizeof(uint64_t)) / per);
+  const size_t ctl = ctl_words(stages_for(tsz)) * sizeof(uint64_t);
+  int cap = (int)((optin - ctl) / per);
   const int wmax = g.left ? kMaxWarpsLeft : kMaxWarps;
   if (cap > wmax) cap = wmax;
   cap &= ~3;
@@ -180,8 +182,9 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   if (nw > cap) nw = cap;
   lp->grid = (int)grid;
   lp->nw = nw;
-  lp->smem = per * nw + kCtlWords * sizeof(uint64_t);
+  lp->smem = per * nw + ctl;
   lp->units = U;
+  lp->mode = mode;
   lp->ua = (int)(U / g.tiles);
   lp->t1 = U % g.tiles;
   return RS_OK;
@@ -268,10 +271,12 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.done = hs ? hs->done : nullptr;
   P.cw = hs ? hs->cw : 1;
   P.ncw = hs ? hs->ncw : 0;
-  P.credit = kStages;
+  P.credit = stages_for(sizeof(T));
+  P.ring_sts = 1;
+  if (const char* ev = getenv("RS_RING_STS")) P.ring_sts = atoi(ev);
   if (const char* ev = getenv("RS_CREDIT")) {
     const int v = atoi(ev);
-    if (v >= 1 && v <= kStages) P.credit = v;
+    if (v >= 1 && v <= stages_for(sizeof(T))) P.credit = v;
   }
   P.len = g.len;
   P.k = g.k;

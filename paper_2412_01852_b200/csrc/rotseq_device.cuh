@@ -32,13 +32,21 @@ constexpr int kR = 2;          // owners (rows) per thread
 #ifndef RS_STAGES
 #define RS_STAGES 2
 #endif
-constexpr int kStages = RS_STAGES;  // ring depth in chunks of K+1 columns (self-fill runs S-1 ahead)
-constexpr int kMaxWarps = 16;  // warps per CTA upper bound (launch bounds)
+#ifndef RS_STAGES_F32
+#define RS_STAGES_F32 3
+#endif
+// ring depth in chunks of K+1 columns (self-fill runs S-1 ahead): fp32 rings are half the
+// size, so they get one more chunk of slack
+__host__ __device__ constexpr int stages_for(size_t tsz) { return tsz == 4 ? RS_STAGES_F32 : RS_STAGES; }
+__host__ __device__ constexpr int ctl_words(int stages) { return stages + 3; }  // per-warp control words
+#ifndef RS_MAX_WARPS
+#define RS_MAX_WARPS 16
+#endif
+constexpr int kMaxWarps = RS_MAX_WARPS;  // warps per CTA upper bound (launch bounds)
 // Left side: the owner-major chunk copies need more registers; 12 warps (170 registers per
 // thread) keep the unrolled body free of spills.
 constexpr int kMaxWarpsLeft = 12;
 constexpr int kTileOwners = 32 * kR;
-constexpr int kCtlWords = kStages + 3;  // per-warp control words (see rs_pipeline_kernel)
 constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
 constexpr int kFlagEvery = RS_FLAG_EVERY;   // hand-off progress is published every 8 blocks (fence cost)
 constexpr size_t kTrashBytes = 32 * kR * 8;  // scratch slot per lane for rows past the matrix
@@ -58,7 +66,9 @@ struct alignas(16) Coef<double, false> {
 };
 template <>
 struct alignas(16) Coef<float, false> {
-  float c, s, pad0, pad1;  // 16-byte records: bulk-copy granularity, one LDS.128
+  // fp32 rotations travel in pairs: lanes 2i and 2i+1 of a wave share one 16-byte record
+  // (c, s, c', s'), so one broadcast LDS.128 serves two rotations (see kPairRecs)
+  float c, s, pad0, pad1;
 };
 template <typename T>
 struct alignas(4 * sizeof(T)) Coef<T, true> {
@@ -68,6 +78,63 @@ struct alignas(4 * sizeof(T)) Coef<T, true> {
 template <typename T>
 using SCoef = Coef<T, false>;
 constexpr int kScaleRecs = 5;  // per block: K+1 = 9 column scales (fp64) in 5 16-byte records
+
+// fp32 rotation records (standard and scaled) hold two lanes each; everything else one.
+// A unit of width kb then stores recs_per_wave(kb) records per wave; units keep the
+// record offsets of the one-lane layout (p0 * nblk * (K+1)), so the pair layout only uses
+// the first part of each unit's region.
+template <typename T, bool REFL>
+constexpr bool kPairRecs = sizeof(T) == 4 && !REFL;
+__host__ __device__ constexpr int recs_per_wave(int kb, bool pair) { return pair ? (kb + 1) / 2 : kb; }
+// the (c, s) of lane l from a wave's records
+// 16-byte record load from shared memory as a volatile asm: keeps the loads where the
+// unrolled body issues them (a few rotation steps ahead of their use) instead of letting
+// the compiler sink them next to the FMAs that consume them
+template <typename CoefT>
+__device__ __forceinline__ CoefT lds_rec(const CoefT* p) {
+  static_assert(sizeof(CoefT) == 16, "16-byte records");
+  CoefT r;
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  if constexpr (sizeof(r.c) == 8) {
+    double x, y;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+    memcpy(&r, &x, 8);
+    memcpy(reinterpret_cast<char*>(&r) + 8, &y, 8);
+  } else {
+    float x, y, z, w;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
+    float v[4] = {x, y, z, w};
+    memcpy(&r, v, 16);
+  }
+  return r;
+}
+template <bool PAIR, typename CoefT>
+__device__ __forceinline__ CoefT lane_coef(const CoefT* __restrict__ wrec, int l) {
+#ifdef RS_ASM_COEF
+  if constexpr (PAIR) {
+    const CoefT r = lds_rec(wrec + (l >> 1));
+    CoefT o = r;
+    if (l & 1) {
+      o.c = r.pad0;
+      o.s = r.pad1;
+    }
+    return o;
+  } else {
+    return lds_rec(wrec + l);
+  }
+#endif
+  if constexpr (PAIR) {
+    const CoefT r = wrec[l >> 1];
+    CoefT o = r;
+    if (l & 1) {
+      o.c = r.pad0;
+      o.s = r.pad1;
+    }
+    return o;
+  } else {
+    return wrec[l];
+  }
+}
 
 // bytes of one per-warp coefficient buffer (two per warp: double buffering)
 template <typename T, bool REFL>
@@ -174,6 +241,61 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 #endif
+// Address-based forms (shared-window u32 addresses computed once per warp) and single-lane
+// forms predicated inside the asm, so the per-block protocol has no divergent branches.
+__device__ __forceinline__ bool mbar_test_a(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+#ifndef RS_X_NOTEST
+  if (mbar_test_a(bar, parity)) return;
+#endif
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "RS_WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra RS_WAITA_%=;\n}" ::"r"(bar),
+      "r"(parity), "r"(kSuspendHintNs)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_if(uint32_t bar, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(bar),
+      "r"((uint32_t)pred)
+      : "memory");
+}
+// "consumed" counters: relaxed stores. Every ring read of the released chunk has already
+// returned its data (the values were consumed by the block's FMAs or stores before the
+// warp barrier), so no later write to the slot can be observed by those reads.
+__device__ __forceinline__ void st_shared_u32_if(uint32_t a, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+#ifdef RS_X_RELCONS
+      "@p st.release.cta.shared::cta.u32 [%0], %1;\n}" ::"r"(a),
+#else
+      "@p st.volatile.shared::cta.u32 [%0], %1;\n}" ::"r"(a),
+#endif
+      "r"(v), "r"((uint32_t)pred)
+      : "memory");
+}
+// coefficient block copy by one lane: arm the barrier with the byte count, start the copy
+__device__ __forceinline__ void coef_copy_if(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %4, 0;\n\t"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+      "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "r"((uint32_t)pred)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
@@ -225,7 +347,10 @@ __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
-  while (ld_acquire_shared(p) < target) __nanosleep(32);
+#ifndef RS_CSLEEP
+#define RS_CSLEEP 32
+#endif
+  while (ld_acquire_shared(p) < target) __nanosleep(RS_CSLEEP);
 }
 __device__ __forceinline__ uint32_t wait_flag(const uint32_t* p, uint32_t target) {
   uint32_t v;
@@ -302,6 +427,7 @@ struct PipeParams {
   int nw;            // warps per CTA (multiple of 4)
   int use_scaled;    // fast fp64: scaled records were packed
   int credit;        // ring credit in chunks (1..S)
+  int ring_sts;      // right side: ring outputs through STS (else the generic store path)
   // host-streaming mode (rs_apply_host_*): A arrives from the host in wave-column chunks
   // of cw columns while the kernel runs, and leaves in the same chunks as soon as every
   // tile's final unit has emitted them. Null pointers: A is resident.
@@ -419,35 +545,52 @@ template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, b
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* islot, T* const (&op)[R], const long long (&ostr)[R],
-                                          uint32_t obase, int b, int len, int Kb, int lane, bool has_in_rt,
+                                          T* obase, int b, int len, int Kb, int lane, bool has_in_rt,
                                           bool has_out_rt) {
-  constexpr uint32_t OSU = (LEFT ? 1 : 32 * R) * sizeof(T);
-  constexpr uint32_t OSR = (LEFT ? 32 * (K + 1) : 32) * sizeof(T);
+  // OUTS: element strides of the output column (u) and row (r) in the shared slot
+  constexpr int OSU = LEFT ? 1 : 32 * R;
+  constexpr int OSR = LEFT ? 32 * (K + 1) : 32;
   constexpr int TR = 32 * R;
   constexpr int NL = EDGE ? K : KB;
   const long long c0 = (long long)b * (K + 1);
   const bool has_in = !EDGE || has_in_rt;
   const bool has_out = !EDGE || has_out_rt;
   // scaled mode: the emitted column is multiplied back by its scale (after the block's records)
-  const T* __restrict__ sc = reinterpret_cast<const T*>(cb + (K + 1) * (EDGE ? Kb : KB));
+  constexpr bool PAIR = kPairRecs<T, REFL>;
+  const int NR = recs_per_wave(EDGE ? Kb : KB, PAIR);  // records per wave
+  const T* __restrict__ sc = reinterpret_cast<const T*>(cb + (K + 1) * NR);
   T* q[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) q[r] = op[r];
+  auto load_col = [&](int u, T (&dst)[R]) {
+    const long long col = c0 + u;
+    if (!EDGE || (has_in && col < len)) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = islot[LEFT ? (lane + 32 * r) * (K + 1) + u : u * TR + lane + 32 * r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r] = T(0);
+    }
+  };
+  T nxt[R];
+  load_col(0, nxt);
+  // coefficient records prefetched CD rotation steps ahead (register queue; the ring index
+  // t % CD is a compile-time constant in the unrolled loops)
+  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
+  constexpr int CD = 4;
+  CoefT cq[CD];
+  if constexpr (!EDGE) {
+#pragma unroll
+    for (int t = 0; t < CD && t < (K + 1) * NL; ++t) cq[t] = lane_coef<PAIR>(cb + (t / NL) * NR, t % NL);
+  }
 #pragma unroll
   for (int u = 0; u <= K; ++u) {
-    // incoming column (LEFT rings are owner-major [owner][K+1]; right rings wave-major)
+    // incoming column (LEFT rings are owner-major [owner][K+1]; right rings wave-major),
+    // loaded one wave ahead so the shared-memory latency overlaps the previous wave
     T nv[R];
-    {
-      const long long col = c0 + u;
-      if (!EDGE || (has_in && col < len)) {
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          nv[r] = islot[LEFT ? (lane + 32 * r) * (K + 1) + u : u * TR + lane + 32 * r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < R; ++r) nv[r] = T(0);
-      }
-    }
+    for (int r = 0; r < R; ++r) nv[r] = nxt[r];
+    if (u < K) load_col(u + 1, nxt);
     // outgoing column (LEFT may stage it in place of the column just read)
     if (has_out) {
       const long long col = c0 - (K + 1) + u;
@@ -456,7 +599,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
         for (int r = 0; r < R; ++r) {
           const T v = SCALED ? mul_rn(w[r][u], sc[u]) : w[r][u];
           if constexpr (OUTS) {
-            st_shared<T>(obase + u * OSU + r * OSR, v);
+            obase[u * OSU + r * OSR] = v;
           } else {
 #ifndef RS_X_NOGSTORE
             *q[r] = v;
@@ -482,7 +625,16 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
         const long long j = c0 + u - 1 - l;
         if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
       }
-      const auto cf = cb[u * (EDGE ? Kb : KB) + l];
+      // interior blocks: the record of step t = u*NL + l was loaded CD steps earlier
+      CoefT cf;
+      if constexpr (EDGE) {
+        cf = lane_coef<PAIR>(cb + u * NR, l);
+      } else {
+        constexpr int NSTEP = (K + 1) * NL;
+        const int t = u * NL + l;
+        cf = cq[t % CD];
+        if (t + CD < NSTEP) cq[t % CD] = lane_coef<PAIR>(cb + ((t + CD) / NL) * NR, (t + CD) % NL);
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if constexpr (SCALED) {
@@ -504,10 +656,411 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
-  constexpr int S = kStages;
+  constexpr int S = stages_for(sizeof(T));
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
-  constexpr int NBAR = kCtlWords;
+  constexpr int NBAR = ctl_words(S);
+
+  const int NW = P.nw;
+  // warp-uniform for the compiler (uniform registers for the per-block protocol operands)
+#ifdef RS_X_NOSHFL
+  const int warp = threadIdx.x >> 5;
+#else
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+#endif
+  const int lane = threadIdx.x & 31;
+  const bool lane0 = lane == 0;
+  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
+
+  T* const A = reinterpret_cast<T*>(P.A);
+  const int len = P.len;
+  const int k = P.k;
+  const int nchunk = P.nchunk;
+  const int nblk = P.nblk;
+  const uint32_t credit = (uint32_t)P.credit;
+  uint64_t* const bar_in = bars + warp * NBAR;  // in-ring of this warp: full[S], consumed, coef[2]
+  uint64_t* const full_in = bar_in;
+  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
+  uint64_t* const cbar = bar_in + S + 1;
+  // position p of a round runs on warp p % NW; the next position on warp + 1
+  const int slot = warp;
+  uint64_t* const full_out = bars + (warp + 1) * NBAR;
+  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
+  T* const rin = ring_sm + (size_t)warp * S * CHUNK;
+  T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
+  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
+  // shared-window addresses of this warp's protocol words and buffers
+  const uint32_t fullin_a = smem_u32(full_in), fullout_a = smem_u32(full_out);
+  const uint32_t consin_a = smem_u32(consumed_in), cbar_a = smem_u32(cbar), cbuf_a = smem_u32(cbuf);
+
+  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
+  const long long npos = cr.g1 - cr.g0;
+  uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
+
+  for (int jr = 0;; ++jr) {
+    const long long pos = (long long)jr * NW + slot;
+    if (pos >= npos) break;
+    const long long g = pos_to_unit(cr, pos);
+    const Unit un = unit_at(g, P.t1, P.ua, k);
+    const long long tile = un.tile;
+    const int p0 = un.p0;
+    const int Kb = un.kb;
+    // the producer of this unit is unit g-1 (same tile, ends at sweep p0); its consumer is
+    // g+1. Ring hand-off when that unit is the neighbouring position of the same round.
+    int src = SRC_GLOBAL, dst = DST_GLOBAL;
+    if (p0 > 0) {
+      src = SRC_FLAG;
+      if (slot > 0 && g - 1 >= cr.g0 && unit_to_pos(cr, g - 1) == pos - 1) src = SRC_RING;
+    }
+    if (p0 + Kb < k) {
+      dst = DST_FLAG;
+      if (slot < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
+    }
+    const bool self = src != SRC_RING;
+
+    T* grow[R];        // element (row r, column 0) of this lane's lines
+    long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long o = tile * TR + lane + 32 * r;
+      const bool ok = o < P.owners;
+      grow[r] = ok ? A + o * P.os : reinterpret_cast<T*>(P.trash) + lane + 32 * r;
+      gcs[r] = ok ? P.cs : 0;
+    }
+    // LEFT coalesced chunk copies: this lane's first element e = lane is owner lo0, column
+    // lv0; each step of 32 elements advances 3 owners + 5 columns (wrapping past K+1)
+    static_assert(32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
+    const int lo0 = lane / (K + 1), lv0 = lane - lo0 * (K + 1);
+    const long long lstep = 3 * P.os + (32 - 3 * (K + 1)) * P.cs;
+    const long long lwrap = P.os - (K + 1) * P.cs;
+    const T* const lbase = A + (tile * TR + lo0) * P.os + lv0 * P.cs;
+    const bool lfull = tile * TR + TR <= P.owners;
+    // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
+    // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
+    const int part = tile < P.t1 ? 1 : 0;
+    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
+    const CoefT* ubase;
+    if constexpr (SCALED) {
+      const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
+      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
+              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
+    } else {
+      ubase = reinterpret_cast<const CoefT*>(P.coef) + (size_t)part * k * nblk * (K + 1) + (size_t)p0 * nblk * (K + 1);
+    }
+    const uint32_t blk_bytes = (uint32_t)(brec * sizeof(CoefT));
+    // one elected lane: WAR fence for the buffer's previous readers, arm, start the copy
+    // The buffer's previous readers are this warp's own LDS, whose values were consumed
+    // before the warp barrier that precedes every issue (no proxy fence needed for WAR).
+    auto issue_coef = [&](int b, uint32_t buf) {
+#ifdef RS_X_OLDCOEF
+      if (lane == 0) {
+        uint64_t* bar = &cbar[buf];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar, blk_bytes);
+        bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
+      }
+#else
+      coef_copy_if(cbuf_a + buf * (uint32_t)CBUF, ubase + (size_t)b * brec, blk_bytes, cbar_a + buf * 8u, lane0);
+#endif
+    };
+    const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
+    const uint32_t* myflag = P.flags + tile * k + p0;
+    uint32_t* const outflag = P.flags + tile * k + p0 + Kb;
+    TraceAcc tacc;
+    tacc.t0 = trace_gtime();
+
+    issue_coef(0, cseq & 1);
+
+    // self-filled input (sweep 0 reads A; a flag hand-off reads A after the producer's
+    // progress flag): cp.async (LDGSTS) straight into this warp's own ring, FA chunks ahead.
+    uint32_t flag_seen = 0;
+    auto fill_chunk = [&](int q) {
+#ifdef RS_X_NOFILL
+      if (src == SRC_GLOBAL) { cp_async_commit(); return; }
+#endif
+      if (src == SRC_FLAG && flag_seen < (uint32_t)q + 1) flag_seen = wait_flag(myflag, (uint32_t)q + 1);
+      if (HS && src == SRC_GLOBAL) {  // host streaming: wait for the copy of these columns
+        long long cend = (long long)q * (K + 1) + K;
+        if (cend > len - 1) cend = len - 1;
+        const uint32_t need = (uint32_t)(cend / P.cw) + 1u;
+        if (flag_seen < need) flag_seen = wait_flag(P.arrived, need);
+      }
+      T* dstp = rin + ((seq0 + (uint32_t)q) % S) * CHUNK;
+      const long long c0 = (long long)q * (K + 1);
+      if constexpr (LEFT) {
+        // owner-major chunk [TR owners][K+1 columns]: element e = i*32 + lane is owner
+        // e/(K+1), column e%(K+1) — consecutive lanes read consecutive columns of one owner
+        // (contiguous in A on the left side) and write consecutive shared words. (owner,
+        // column) and the address advance incrementally (e += 32: +3 owners, +5 columns).
+        int v = lv0;
+        const T* sp = lbase + c0 * P.cs;
+        if (lfull && c0 + K < len) {
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            cp_async_elem(dstp + i * 32 + lane, sp, true);
+            v += 32 - 3 * (K + 1);
+            sp += lstep;
+            if (v >= K + 1) v -= K + 1, sp += lwrap;
+          }
+        } else {
+          int ol = lo0;
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            const bool ok = tile * TR + ol < P.owners && c0 + v < len;
+            cp_async_elem(dstp + i * 32 + lane, ok ? sp : A, ok);
+            v += 32 - 3 * (K + 1);
+            ol += 3;
+            sp += lstep;
+            if (v >= K + 1) v -= K + 1, ++ol, sp += lwrap;
+          }
+        }
+        cp_async_commit();
+        return;
+      }
+      const T* sp[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) sp[r] = grow[r] + c0 * gcs[r];
+      if (c0 + K < len) {
+#pragma unroll
+        for (int v = 0; v <= K; ++v) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            cp_async_elem(dstp + v * TR + lane + 32 * r, sp[r], true);
+            sp[r] += gcs[r];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v <= K; ++v) {
+          const bool cv = c0 + v < len;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            cp_async_elem(dstp + v * TR + lane + 32 * r, cv ? sp[r] : grow[r], cv);
+            sp[r] += gcs[r];
+          }
+        }
+      }
+      cp_async_commit();
+    };
+    // Self-filled chunks still arrive on full_in (nobody waits on them) so the barrier's
+    // phase count stays equal to the chunk sequence number for ring-fed rounds later on.
+    unsigned long long tc = trace_clock();
+    if (self) {
+      fill_chunk(0);
+      if (FA >= 2 && 1 < nchunk) fill_chunk(1);
+      if (FA >= 2 && 1 < nchunk)
+        cp_async_wait_group<1>();
+      else
+        cp_async_wait_group<0>();
+      __syncwarp();
+      mbar_arrive_if(fullin_a + (seq0 % S) * 8u, lane0);
+    }
+    tacc.c[0] += trace_clock() - tc;
+
+    T w[R][K + 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int s = 0; s <= K; ++s) w[r][s] = T(0);
+
+    const bool outring = dst == DST_RING;
+    int done_sig = 0;  // host streaming: chunks already released by this (final) unit
+    // incremental protocol state: in-ring slot / phase of the chunk read by block b
+    // (iseq = seq0 + b), coefficient buffer / phase (cseq)
+    uint32_t ib = seq0 % S, iph = (seq0 / S) & 1u;
+    uint32_t cbi = cseq & 1u, cph = (cseq >> 1) & 1u;
+    // One block: protocol + compute. KB / EDGE are compile-time so the interior loop
+    // carries no per-block branches beyond this unit's hand-off protocol.
+    auto block = [&](int b, auto kb_c, auto edge_c) {
+      constexpr int KB = decltype(kb_c)::value;
+      constexpr bool EDGE = decltype(edge_c)::value;
+      unsigned long long t0 = trace_clock();
+#ifdef RS_X_NOCOEF
+      if (b + 1 < nblk && b < 1) issue_coef(b + 1, cbi ^ 1u);
+#else
+      if (b + 1 < nblk) issue_coef(b + 1, cbi ^ 1u);
+#endif
+      const bool has_in = !EDGE || b < nchunk;
+      const bool has_out = !EDGE || b >= 1;
+      if (self && b + FA < nchunk) fill_chunk(b + FA);
+      unsigned long long t1 = trace_clock();
+      const uint32_t iseq = seq0 + (uint32_t)b;
+      const uint32_t ob = ib == 0 ? (uint32_t)(S - 1) : ib - 1u;  // slot of chunk oseq = iseq - 1
+      const T* islot = rin + ib * CHUNK;
+      const uint32_t oseq = iseq - 1u;
+      // output: the consumer's ring slot or (LEFT) the staging slot, by shared address;
+      // right side to A through generic pointers (column stride gcs)
+      T* op[R];
+      long long ostr[R];
+      // LEFT, output to A: stage the outgoing chunk in the input slot just read (the last
+      // block, which has no input, reuses the previous block's slot) and copy it out below
+      const uint32_t stage_i = b < nchunk ? ib : ob;
+      T* stage = rin + stage_i * CHUNK;
+      // (pointers derived from the shared-memory window: plain STS with alias analysis)
+      T* obase = nullptr;
+      if (outring) {
+        obase = rout + ob * CHUNK + lane * (LEFT ? K + 1 : 1);
+      } else if (LEFT) {
+        obase = rin + stage_i * CHUNK + lane * (K + 1);
+      } else {
+        const long long cb0 = (long long)b * (K + 1) - (K + 1);
+#pragma unroll
+        for (int r = 0; r < R; ++r) op[r] = grow[r] + cb0 * gcs[r], ostr[r] = gcs[r];
+      }
+#ifdef RS_X_NOCOEF
+      if (b < 2) mbar_wait_a(cbar_a + cbi * 8u, cph);
+#else
+      mbar_wait_a(cbar_a + cbi * 8u, cph);
+#endif
+      unsigned long long t2 = trace_clock();
+#ifndef RS_X_NOSYNC
+      if (!self && has_in) mbar_wait_a(fullin_a + ib * 8u, iph);
+#endif
+      unsigned long long t3 = trace_clock();
+      // ring credit: the producer runs at most `credit` chunks ahead of its consumer
+#ifndef RS_X_NOSYNC
+      if (outring && has_out && oseq >= credit) wait_count(consumed_out, oseq - credit + 1u);
+#endif
+      unsigned long long t4 = trace_clock();
+      {
+        const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + cbi * CBUF);
+        if (LEFT || outring) {
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, obase, b, len, Kb,
+                                                                          lane, b < nchunk, b >= 1);
+        } else {
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, nullptr, b, len, Kb,
+                                                                           lane, b < nchunk, b >= 1);
+        }
+      }
+      __syncwarp();
+      if (LEFT && !outring && has_out) {  // copy the staged chunk to A, columns contiguous
+        const long long cb0 = (long long)(b - 1) * (K + 1);
+        int v = lv0;
+        T* dp = const_cast<T*>(lbase) + cb0 * P.cs;
+        if (lfull && cb0 + K < len) {
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            *dp = stage[i * 32 + lane];
+            v += 32 - 3 * (K + 1);
+            dp += lstep;
+            if (v >= K + 1) v -= K + 1, dp += lwrap;
+          }
+        } else {
+          int ol = lo0;
+#pragma unroll
+          for (int i = 0; i < R * (K + 1); ++i) {
+            if (tile * TR + ol < P.owners && cb0 + v < len) *dp = stage[i * 32 + lane];
+            v += 32 - 3 * (K + 1);
+            ol += 3;
+            dp += lstep;
+            if (v >= K + 1) v -= K + 1, ++ol, dp += lwrap;
+          }
+        }
+        __syncwarp();
+      }
+      unsigned long long t5 = trace_clock();
+      // LEFT global output: the last block stages in the slot of chunk nchunk-1, so that
+      // slot is released one block later (as nchunk, i.e. iseq of the last block)
+#ifdef RS_X_OLDPOST
+      if (lane == 0) {
+        if (LEFT && !outring) {
+          if (has_in && b + 1 < nchunk) st_release_shared(consumed_in, iseq + 1u);
+          if (b == nchunk) st_release_shared(consumed_in, iseq);
+        } else if (has_in) {
+          st_release_shared(consumed_in, iseq + 1u);
+        }
+        if (outring && has_out) mbar_arrive(&full_out[ob]);
+      }
+#else
+      if (LEFT && !outring) {
+        if (has_in && b + 1 < nchunk) st_shared_u32_if(consin_a, iseq + 1u, lane0);
+        if (b == nchunk) st_shared_u32_if(consin_a, iseq, lane0);
+      } else if (has_in) {
+        st_shared_u32_if(consin_a, iseq + 1u, lane0);
+      }
+      if (outring && has_out) mbar_arrive_if(fullout_a + ob * 8u, lane0);
+#endif
+      if (dst == DST_FLAG && has_out &&
+          (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b >= nblk - RS_FLAG_TAIL)) {
+        if (lane0) {
+          // the warp barrier above orders every lane's stores before lane 0's gpu-scope
+          // fence; the release store then publishes "chunks 0..b-1 are in A"
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          st_release(outflag, (uint32_t)b);
+        }
+      }
+      if (HS && dst == DST_GLOBAL && has_out && lane0) {  // host streaming: release finished chunks
+        long long e = (long long)b * (K + 1) - 1;  // last column emitted by this block
+        if (e > len - 1) e = len - 1;
+        const int nd = e == len - 1 ? P.ncw : (int)((e + 1) / P.cw);
+        if (nd > done_sig) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          for (; done_sig < nd; ++done_sig) atomicAdd(P.done + done_sig, 1u);
+        }
+      }
+      // advance the in-ring slot (the next block reads chunk iseq + 1)
+      const uint32_t nib = ib + 1u == (uint32_t)S ? 0u : ib + 1u;
+      if (self && b + 1 < nchunk) {  // the chunk read by the next block has landed
+        if (FA >= 2 && b + 2 < nchunk)
+          cp_async_wait_group<1>();
+        else
+          cp_async_wait_group<0>();
+        __syncwarp();
+        mbar_arrive_if(fullin_a + nib * 8u, lane0);
+      }
+      if (nib == 0) iph ^= 1u;
+      ib = nib;
+#ifdef RS_X_NOCOEF
+      if (b < 2) { ++cseq; cbi ^= 1u; if (cbi == 0) cph ^= 1u; }
+#else
+      ++cseq;
+      cbi ^= 1u;
+      if (cbi == 0) cph ^= 1u;
+#endif
+      unsigned long long t6 = trace_clock();
+      tacc.c[0] += t1 - t0;
+      tacc.c[1] += t2 - t1;
+      tacc.c[2] += t3 - t2;
+      tacc.c[3] += t4 - t3;
+      tacc.c[4] += t5 - t4;
+      tacc.c[5] += t6 - t5;
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    using I8 = std::integral_constant<int, K>;
+    const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
+    const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
+    block(0, I8{}, T_{});
+    switch (Kb) {
+      case 8: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 8>{}, F_{}); break;
+      case 7: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 7>{}, F_{}); break;
+      case 6: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 6>{}, F_{}); break;
+      case 5: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 5>{}, F_{}); break;
+      case 4: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 4>{}, F_{}); break;
+      case 3: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 3>{}, F_{}); break;
+      case 2: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 2>{}, F_{}); break;
+      default: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 1>{}, F_{}); break;
+    }
+    for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
+    trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
+  }
+}
+
+// Right side: the original per-block protocol (generic-pointer output, lane-0 branches);
+// it schedules the unrolled body better than the lean protocol under the 128-register
+// budget of 16-warp CTAs.
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED, bool HS, bool LEFT>
+__device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsigned char* smem_raw) {
+  static_assert(!LEFT, "right-side protocol");
+  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
+  constexpr int TR = 32 * R;
+  constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
+  constexpr int S = stages_for(sizeof(T));
+  constexpr int FA = S - 1;  // self-fill distance in chunks
+  static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
+  constexpr int NBAR = ctl_words(S);
 
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
@@ -578,7 +1131,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
     // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
     const int part = tile < P.t1 ? 1 : 0;
-    const int brec = Kb * (K + 1) + (SCALED ? kScaleRecs : 0);
+    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
     const CoefT* ubase;
     if constexpr (SCALED) {
       const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
@@ -758,12 +1311,14 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       unsigned long long t4 = trace_clock();
       {
         const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF);
-        if (LEFT || outring) {
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, smem_u32(op[0]), b,
-                                                                          len, Kb, lane, b < nchunk, b >= 1);
+        // ring output by STS (default) or through the generic store path shared with A
+        // outputs (P.ring_sts = 0: one loop body per unit width)
+        if (outring && P.ring_sts) {
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, op[0], b, len, Kb,
+                                                                          lane, b < nchunk, b >= 1);
         } else {
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, 0u, b, len, Kb,
-                                                                           lane, b < nchunk, b >= 1);
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, nullptr, b, len,
+                                                                           Kb, lane, b < nchunk, b >= 1);
         }
       }
       __syncwarp();
@@ -862,12 +1417,13 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   }
 }
 
+
 // HS: host-streaming variant (rs_apply_host_*), a separate instantiation so the resident
 // path carries none of its checks
 template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
 __global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
-  constexpr int S = kStages;
-  constexpr int NBAR = kCtlWords;
+  constexpr int S = stages_for(sizeof(T));
+  constexpr int NBAR = ctl_words(S);
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
@@ -887,11 +1443,19 @@ __global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs
   // fast mode: the scaled form, unless the pack found coefficients outside its safe range
   if constexpr (!STRICT) {
     if (P.use_scaled && *P.unsafe == 0u) {
-      pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
+      if constexpr (LEFT) {
+        pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
+      } else {
+        pipeline_units_right<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
+      }
       return;
     }
   }
-  pipeline_units<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
+  if constexpr (LEFT) {
+    pipeline_units<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
+  } else {
+    pipeline_units_right<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -920,7 +1484,9 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
     const int p0 = sweep_start(i, ut, k);
     const int kb = sweep_start(i + 1, ut, k) - p0;
     const int l = p - p0;
-    Coef<T, REFL>* dst = out + (size_t)part * k * per_p + (size_t)p0 * per_p + l;
+    constexpr bool PAIR = kPairRecs<T, REFL>;
+    const int nr = recs_per_wave(kb, PAIR);
+    Coef<T, REFL>* dst = out + (size_t)part * k * per_p + (size_t)p0 * per_p + (PAIR ? l / 2 : l);
     for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < per_p; x += gridDim.x * blockDim.x) {
       const int b = x / (K + 1);
       const int u = x - b * (K + 1);
@@ -941,7 +1507,13 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
           cf.s = s;
         }
       }
-      dst[((size_t)b * (K + 1) + u) * kb] = cf;
+      if constexpr (PAIR) {
+        T* h = reinterpret_cast<T*>(dst + ((size_t)b * (K + 1) + u) * nr) + 2 * (l & 1);
+        h[0] = cf.c;
+        h[1] = cf.s;
+      } else {
+        dst[((size_t)b * (K + 1) + u) * kb] = cf;
+      }
     }
   }
 }
@@ -991,7 +1563,9 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     if (i >= ut) continue;
     const int p0 = sweep_start(i, ut, k);
     const int kb = sweep_start(i + 1, ut, k) - p0;
-    const int brec = kb * (K + 1) + kScaleRecs;
+    constexpr bool PAIR = kPairRecs<T, REFL>;
+    const int nr = recs_per_wave(kb, PAIR);
+    const int brec = nr * (K + 1) + kScaleRecs;
     SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
                       (size_t)i * nblk * kScaleRecs;
     double sa = 1, sb = 1;  // running scales of columns j and j+1
@@ -1014,7 +1588,13 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
         SCoef<T> rec{};
         rec.c = (T)t1;
         rec.s = (T)-t2;
-        ubase[(size_t)b * brec + u * kb + l] = rec;
+        if constexpr (PAIR) {
+          T* h = reinterpret_cast<T*>(ubase + (size_t)b * brec + u * nr + l / 2) + 2 * (l & 1);
+          h[0] = rec.c;
+          h[1] = rec.s;
+        } else {
+          ubase[(size_t)b * brec + u * kb + l] = rec;
+        }
         sa *= c;
         sb *= REFL ? -c : c;
         if (j + 1 <= len - 2) {  // rotation (j+1, p) touches column j+1 as its x
@@ -1026,7 +1606,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     }
     // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
     const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
-    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)kb * (K + 1))[ue] = (T)sa;
+    if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)nr * (K + 1))[ue] = (T)sa;
     if (bad) atomicOr(unsafe, 1u);
   }
 }

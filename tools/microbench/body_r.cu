@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(NT, 1) body(double* out, int nblocks, int cw) 
     double th = 0.001 * i; coef[i] = make_double2(0.1 * sin(th), -0.1 * cos(th));
   }
   double* myio = io + warp * 32 * R * (K + 1);
+  const double* inio = io + (warp ^ 1) * 32 * R * (K + 1);  // another warp's slot: no store-to-load forwarding
   for (int i = lane; i < 32 * R * (K + 1); i += 32) myio[i] = 1.0 + i;
   __syncthreads();
   double w[R][K + 1];
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(NT, 1) body(double* out, int nblocks, int cw) 
     for (int u = 0; u <= K; ++u) {
       double nv[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) nv[r] = myio[(((u + 3) % (K + 1)) * R + r) * 32 + lane];
+      for (int r = 0; r < R; ++r) nv[r] = *(volatile const double*)&inio[(((u + 3) % (K + 1)) * R + r) * 32 + lane];
       const double sc = cb[(K + 1) * KB + u / 2].x;
 #pragma unroll
       for (int r = 0; r < R; ++r) myio[(u * R + r) * 32 + lane] = w[r][u] * sc;
@@ -83,9 +84,8 @@ void run() {
   cudaFree(o);
 }
 int main() {
-  run<8, 7, 2, 384, 0>(); run<8, 7, 2, 384, 1>(); run<8, 7, 2, 384, 2>();
-  run<8, 7, 2, 256, 0>(); run<8, 7, 2, 256, 1>(); run<8, 7, 2, 256, 2>();
-  run<8, 7, 4, 256, 0>(); run<8, 7, 4, 256, 1>(); run<8, 7, 4, 256, 2>();
-  run<8, 7, 4, 128, 0>(); run<8, 7, 4, 128, 1>(); run<8, 7, 4, 128, 2>();
+  run<8, 7, 2, 384, 0>(); run<8, 7, 2, 512, 0>(); run<8, 7, 2, 256, 0>();
+  run<8, 7, 3, 384, 0>(); run<8, 7, 3, 256, 0>();
+  run<8, 7, 4, 256, 0>(); run<8, 8, 4, 256, 0>(); run<8, 8, 3, 256, 0>();
   return 0;
 }
