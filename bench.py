@@ -273,7 +273,8 @@ def main():
             dist.broadcast(dS, src=0)
 
     broadcast_cs()
-    packed = PackedSequence((dC, dS), (m_loc, n_loc), side=w.side, order=w.order, dtype=tdtype, device=dev)
+    packed = PackedSequence((dC, dS), (m_loc, n_loc), side=w.side, order=w.order, dtype=tdtype, device=dev,
+                            fast_only=fast)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 

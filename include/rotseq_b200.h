@@ -111,6 +111,14 @@ rs_status rs_pack_f64(const double* C, const double* S, int64_t ldcs, int64_t m,
                       int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
 rs_status rs_pack_f32(const float* C, const float* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
                       int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
+/* Fast-mode-only pack: as rs_pack_*, but the standard (unscaled) records are written only
+ * when the scaled form is out of range for these coefficients — the per-call fast path's
+ * pack. The workspace may then only be applied with strict = 0 (the Python mirror,
+ * PackedSequence(fast_only=True), enforces it). */
+rs_status rs_pack_fast_f64(const double* C, const double* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                           int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
+rs_status rs_pack_fast_f32(const float* C, const float* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                           int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream);
 rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,
                               int kind, int strict, void* workspace, size_t workspace_bytes, void* stream);
 rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,

@@ -41,6 +41,8 @@ EXPORTS = (
     "rs_plan_info",
     "rs_pack_f64",
     "rs_pack_f32",
+    "rs_pack_fast_f64",
+    "rs_pack_fast_f32",
     "rs_apply_packed_f64",
     "rs_apply_packed_f32",
     "rs_apply_host_f64",
@@ -75,7 +77,7 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [i32] + apply_args
-    for name in ("rs_pack_f64", "rs_pack_f32"):
+    for name in ("rs_pack_f64", "rs_pack_f32", "rs_pack_fast_f64", "rs_pack_fast_f32"):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [vp, vp, i64, i64, i64, i64, i32, i32, i32, vp, sz, vp]

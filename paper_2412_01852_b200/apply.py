@@ -333,11 +333,15 @@ class PackedSequence:
     blocking.py:479-515; the paper's rs_kernel_v2): ``pack`` runs the
     repack kernel into a persistent workspace, ``apply`` runs only the pipeline kernel
     on a device-resident A. Shape, side, order and kind are fixed at construction.
+    ``fast_only=True`` packs for fast-mode application only (``rs_pack_fast_*``: the
+    standard records are written only when the scaled form is out of range), which
+    makes every re-pack cheaper; ``apply(fast=False)`` is then refused.
     """
 
     def __init__(self, seq, shape, kind=TransformKind.ROTATION, side=Side.RIGHT, order=Order.FORWARD,
-                 dtype=None, device=None, stream=None):
+                 dtype=None, device=None, stream=None, fast_only=False):
         torch = _torch()
+        self.fast_only = bool(fast_only)
         self.kind = _as_enum(kind, TransformKind, "kind")
         self.side = _as_enum(side, Side, "side")
         self.order = _as_enum(order, Order, "order")
@@ -381,7 +385,10 @@ class PackedSequence:
             C, S = C.t().contiguous().t(), S.t().contiguous().t()
         ldcs = int(C.stride(1)) if self.k > 1 else max(self.length - 1, 1)
         lib = _lib.load()
-        fn = lib.rs_pack_f64 if self.f64 else lib.rs_pack_f32
+        if self.fast_only:
+            fn = lib.rs_pack_fast_f64 if self.f64 else lib.rs_pack_fast_f32
+        else:
+            fn = lib.rs_pack_f64 if self.f64 else lib.rs_pack_f32
         with torch.cuda.device(self.device):
             st = fn(C.data_ptr(), S.data_ptr(), ldcs, self.m, self.n, self.k, self._side, self._order, self._kind,
                     self.workspace.data_ptr(), self.workspace.numel(), self._stream(stream))
@@ -396,6 +403,8 @@ class PackedSequence:
             raise ValueError(f"A must have shape {(self.m, self.n)}, got {tuple(A.shape)}")
         if self.m > 1 and A.stride(0) != 1:
             raise ValueError("A must be column-major (first stride 1)")
+        if self.fast_only and not fast:
+            raise ValueError("this PackedSequence was packed fast_only; apply it with fast=True")
         lda = int(A.stride(1)) if self.n > 1 else max(self.m, 1)
         lib = _lib.load()
         fn = lib.rs_apply_packed_f64 if self.f64 else lib.rs_apply_packed_f32

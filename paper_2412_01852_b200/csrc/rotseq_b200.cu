@@ -199,7 +199,7 @@ struct HostStream {
 
 template <typename T, bool REFL>
 rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs, int rev, void* ws,
-                      cudaStream_t st, bool scaled) {
+                      cudaStream_t st, bool scaled, bool std_only_if_unsafe = false) {
   using CoefT = Coef<T, REFL>;
   CoefT* coef = reinterpret_cast<CoefT*>(ws);
   LaunchPlan lp;  // the unit partition of the sweeps comes from the launch plan
@@ -211,13 +211,14 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   if (bx > 64) bx = 64;
   const int rows = nparts * g.k;
   const int by = rows < 65535 ? rows : 65535;
-  rs_pack_kernel<T, REFL><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k, g.nblk,
-                                                                             lp.ua, nparts, rev);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  {
-    if (scaled) {
+  // Scaled records first (fast mode); the standard records are the fallback the pipeline
+  // uses when the scaled form is out of range, so a per-call pack (std_only_if_unsafe)
+  // lets the standard pack kernel exit at once when the scaled records are safe. The
+  // resident pack (rs_pack_*) always writes both: strict or fast is chosen per apply.
+  uint32_t* unsafe = nullptr;
+  if (scaled) {
     unsigned char* base = reinterpret_cast<unsigned char*>(ws);
-    uint32_t* unsafe = reinterpret_cast<uint32_t*>(base + g.coef_bytes + g.flags_only);
+    unsafe = reinterpret_cast<uint32_t*>(base + g.coef_bytes + g.flags_only);
     cudaError_t e0 = cudaMemsetAsync(unsafe, 0, sizeof(uint32_t), st);
     if (e0 != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e0));
     const int srows = nparts * (lp.ua + 1);
@@ -225,8 +226,10 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
     rs_pack_scaled_kernel<T, REFL><<<dim3((unsigned)((g.len + 127) / 128), (unsigned)sy), 128, 0, st>>>(
         reinterpret_cast<SCoef<T>*>(base + g.std_bytes), C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts, rev, unsafe);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
   }
+  rs_pack_kernel<T, REFL><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(
+      coef, C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts, rev, scaled && std_only_if_unsafe ? unsafe : nullptr);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
   return RS_OK;
@@ -359,7 +362,7 @@ rs_status check_workspace(const Geometry& g, void* ws, size_t bytes) {
 
 template <typename T>
 rs_status pack_impl(const T* C, const T* S, int64_t ldcs, int64_t m, int64_t n, int64_t k, int side, int order,
-                    int kind, void* ws, size_t bytes, void* stream) {
+                    int kind, void* ws, size_t bytes, void* stream, bool fast_only = false) {
   Geometry g;
   const int dtype = sizeof(T) == 8 ? RS_DTYPE_F64 : RS_DTYPE_F32;
   rs_status rc = validate(m, n, m > 1 ? m : 1, ldcs, k, side, order, kind, dtype, true, &g);
@@ -369,8 +372,10 @@ rs_status pack_impl(const T* C, const T* S, int64_t ldcs, int64_t m, int64_t n, 
   if (rc != RS_OK) return rc;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int rev = order == RS_ORDER_REVERSE;
-  return kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, true)
-                                   : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, true);
+  // fast_only: the per-call fast path's pack (the scaled form unless it is disabled)
+  const bool scaled = !fast_only || !scaled_disabled();
+  return kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, scaled, fast_only)
+                                   : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, scaled, fast_only);
 }
 
 template <typename T>
@@ -421,8 +426,8 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
     return fail(RS_EINVAL, "workspace must be 256-byte aligned");
   }
   const bool scaled = !strict && !scaled_disabled();
-  rs_status rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, scaled)
-                                           : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, scaled);
+  rs_status rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, C, S, ldcs, rev, ws, st, scaled, true)
+                                           : launch_pack<T, false>(g, C, S, ldcs, rev, ws, st, scaled, true);
   if (rc == RS_OK) rc = run_dispatch<T>(g, A, rev, kind, strict, ws, st);
   if (owned) {
     cudaError_t e = cudaFreeAsync(ws, st);
@@ -670,8 +675,8 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   mark(st, "pack_start");
   if (e == cudaSuccess) {
     const bool scaled = !strict && !scaled_disabled();
-    rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, dC, dS, (long long)lc, rev, ws, st, scaled)
-                                   : launch_pack<T, false>(g, dC, dS, (long long)lc, rev, ws, st, scaled);
+    rc = kind == RS_KIND_REFLECTOR ? launch_pack<T, true>(g, dC, dS, (long long)lc, rev, ws, st, scaled, true)
+                                   : launch_pack<T, false>(g, dC, dS, (long long)lc, rev, ws, st, scaled, true);
     mark(st, "kernel_start");
     if (rc == RS_OK) rc = run_dispatch<T>(g, dA, rev, kind, strict, ws, st, &hs);
     mark(st, "kernel_end");
@@ -837,6 +842,16 @@ rs_status rs_pack_f32(const float* C, const float* S, int64_t ldcs, int64_t m, i
                       int order, int kind, void* workspace, size_t workspace_bytes, void* stream) {
   g_err.clear();
   return pack_impl<float>(C, S, ldcs, m, n, k, side, order, kind, workspace, workspace_bytes, stream);
+}
+rs_status rs_pack_fast_f64(const double* C, const double* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                           int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return pack_impl<double>(C, S, ldcs, m, n, k, side, order, kind, workspace, workspace_bytes, stream, true);
+}
+rs_status rs_pack_fast_f32(const float* C, const float* S, int64_t ldcs, int64_t m, int64_t n, int64_t k,
+                           int side, int order, int kind, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  return pack_impl<float>(C, S, ldcs, m, n, k, side, order, kind, workspace, workspace_bytes, stream, true);
 }
 rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order, int kind,
                               int strict, void* workspace, size_t workspace_bytes, void* stream) {

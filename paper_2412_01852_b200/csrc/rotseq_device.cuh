@@ -1470,8 +1470,12 @@ __global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs
 template <typename T, bool REFL>
 __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
                                                       const T* __restrict__ Sm, long long ldcs, int len, int k,
-                                                      int nblk, int ua, int nparts, int rev) {
+                                                      int nblk, int ua, int nparts, int rev,
+                                                      const uint32_t* __restrict__ only_if_unsafe) {
   constexpr int K = kK;
+  // fast mode packs the scaled records first; the standard records are only the fallback
+  // for coefficients outside the scaled form's safe range
+  if (only_if_unsafe != nullptr && *only_if_unsafe == 0u) return;
   const int per_p = nblk * (K + 1);
   for (int row = blockIdx.y; row < nparts * k; row += gridDim.y) {
     const int part = row / k;

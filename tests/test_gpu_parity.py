@@ -234,6 +234,33 @@ def test_device_tensor_and_packed_resident_mode(cuda, oracle_mod):
     assert_bitwise(ref, dB.cpu().numpy())
 
 
+@pytest.mark.gpu
+def test_packed_fast_only_matches_per_call_fast_path(cuda):
+    """PackedSequence(fast_only=True) (rs_pack_fast_*) skips the standard records when the
+    scaled form is safe: its result equals the per-call fast path bit for bit, for safe
+    coefficients and for quarter turns (c = 0: standard fallback), and strict application
+    of a fast-only pack is refused."""
+    import torch
+
+    from paper_2412_01852_b200 import PackedSequence, apply_device, make_inputs
+
+    for quarter in (False, True):
+        A0, seq = make_inputs(200, 150, 21, 5)
+        C, S = seq.C.copy(order="F"), seq.S.copy(order="F")
+        if quarter:
+            C[7, 3], S[7, 3] = 0.0, 1.0
+        dC, dS = torch.from_numpy(C).to(cuda), torch.from_numpy(S).to(cuda)
+        dA = torch.from_numpy(A0.copy(order="F")).to(cuda)
+        dB = torch.from_numpy(A0.copy(order="F")).to(cuda)
+        packed = PackedSequence((dC, dS), dA.shape, device=cuda, fast_only=True)
+        packed.apply(dA, fast=True)
+        apply_device(dB, (dC, dS), fast=True)
+        torch.cuda.synchronize()
+        assert_bitwise(dB.cpu().numpy(), dA.cpu().numpy())
+        with pytest.raises(ValueError, match="fast_only"):
+            packed.apply(dA, fast=False)
+
+
 def test_pinned_host_tensor_path(cuda, oracle_mod):
     import torch
 
