@@ -39,6 +39,9 @@ constexpr int kR = 2;          // owners (rows) per thread
 // size, so they get one more chunk of slack
 __host__ __device__ constexpr int stages_for(size_t tsz) { return tsz == 4 ? RS_STAGES_F32 : RS_STAGES; }
 __host__ __device__ constexpr int ctl_words(int stages) { return stages + 3; }  // per-warp control words
+#ifndef RS_RIGHT_LEAN
+#define RS_RIGHT_LEAN 0
+#endif
 #ifndef RS_MAX_WARPS
 #define RS_MAX_WARPS 16
 #endif
@@ -1443,7 +1446,7 @@ __global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs
   // fast mode: the scaled form, unless the pack found coefficients outside its safe range
   if constexpr (!STRICT) {
     if (P.use_scaled && *P.unsafe == 0u) {
-      if constexpr (LEFT) {
+      if constexpr (LEFT || RS_RIGHT_LEAN) {
         pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
       } else {
         pipeline_units_right<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
@@ -1451,7 +1454,7 @@ __global__ void __launch_bounds__((LEFT ? kMaxWarpsLeft : kMaxWarps) * 32, 1) rs
       return;
     }
   }
-  if constexpr (LEFT) {
+  if constexpr (LEFT || RS_RIGHT_LEAN) {
     pipeline_units<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
   } else {
     pipeline_units_right<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
