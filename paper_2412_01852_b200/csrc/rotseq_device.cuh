@@ -1575,19 +1575,32 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     const int brec = nr * (K + 1) + kScaleRecs;
     SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
                       (size_t)i * nblk * kScaleRecs;
+    // the unit's coefficients of rotations (j-1, p), (j, p), (j+1, p), loaded up front
+    // (independent loads in flight together; only c is needed for the neighbours)
+    double cl[kK], cj[kK], sj[kK], cr[kK];
+#pragma unroll
+    for (int l = 0; l < kK; ++l) {
+      cl[l] = cj[l] = cr[l] = 1.0;
+      sj[l] = 0.0;
+      if (l < kb) {
+        double sd;
+        if (j >= 1) coef(j - 1, p0 + l, cl[l], sd);
+        if (j <= len - 2) coef(j, p0 + l, cj[l], sj[l]);
+        if (j + 1 <= len - 2) coef(j + 1, p0 + l, cr[l], sd);
+      }
+    }
     double sa = 1, sb = 1;  // running scales of columns j and j+1
     bool bad = false;
-    for (int l = 0; l < kb; ++l) {
-      const int p = p0 + l;
-      double c, s;
-      if (j >= 1) {  // rotation (j-1, p) touched column j as its y
-        coef(j - 1, p, c, s);
-        sa *= REFL ? -c : c;
-      }
+#pragma unroll
+    for (int l = 0; l < kK; ++l) {
+      if (l >= kb) break;
+      if (j >= 1) sa *= REFL ? -cl[l] : cl[l];  // rotation (j-1, p) touched column j as its y
       if (j <= len - 2) {
-        coef(j, p, c, s);
-        const double t1 = s * sb / (c * sa);
-        const double t2 = s * sa / (c * sb);
+        const double c = cj[l], s = sj[l];
+        // tau1 = s*sb / (c*sa), tau2 = s*sa / (c*sb), with one division
+        const double q = 1.0 / (c * sa * sb);
+        const double t1 = s * sb * sb * q;
+        const double t2 = s * sa * sa * q;
         bad |= !(c != 0.0) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
         // rotation (j, p) runs in block b at wave u with b(K+1) + u = j + 1 + l
         const int bu = j + 1 + l;
@@ -1604,10 +1617,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
         }
         sa *= c;
         sb *= REFL ? -c : c;
-        if (j + 1 <= len - 2) {  // rotation (j+1, p) touches column j+1 as its x
-          coef(j + 1, p, c, s);
-          sb *= c;
-        }
+        if (j + 1 <= len - 2) sb *= cr[l];  // rotation (j+1, p) touches column j+1 as its x
       }
       bad |= !(fabs(sa) >= lo && fabs(sa) <= hi) || !(fabs(sb) >= lo && fabs(sb) <= hi);
     }
