@@ -166,7 +166,11 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   // Few units per sub-partition: U = 4*G*q balances every sub-partition exactly (widths
   // k/u_t, mixed). Many units (several rounds): full-width units (U = umin) keep every
   // round's per-SMSP load equal and the residual imbalance (< 1/q) is small.
-  int mode = q >= 8 ? 2 : 1;
+  // Mode 1 also loses when its extra units barely narrow them (average width > 7.5 of 8):
+  // a tile then mixes 7- and 8-wide units and its chain runs at the 8-wide units' pace
+  // (measured: 8192 x 2048 x 256, the 8-GPU shard of config 3: 18.9 -> 20.7 TF/s).
+  const double w1 = (double)g.k * (double)g.tiles / (double)(4 * grid * q);
+  int mode = (q >= 8 || w1 > 7.5) ? 2 : 1;
   if (const char* ev = getenv("RS_PLAN_MODE")) {
     const int v = atoi(ev);
     if (v == 1 || v == 2) mode = v;

@@ -58,7 +58,8 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
     G = max(1, min(G, -(-umin // 4)))
     q = -(-umin // (4 * G))
     if mode == 0:
-        mode = 2 if q >= 8 else 1
+        w1 = g.k * g.tiles / (4 * G * q)
+        mode = 2 if (q >= 8 or w1 > 7.5) else 1
     U = 4 * G * q if mode == 1 else umin
     U = min(U, g.tiles * g.k)
     nmax = -(-U // G)
