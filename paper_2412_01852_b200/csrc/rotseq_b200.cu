@@ -116,7 +116,7 @@ struct LaunchPlan {
   long long units = 0;
   int ua = 0;
   long long t1 = 0;
-  int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units, several rounds
+  int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units; 3: aligned
 };
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec) {
@@ -153,6 +153,44 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   if (const char* ev = getenv("RS_DEBUG_GRID")) {
     const long long v = atoll(ev);
     if (v >= 1 && v < grid) grid = v;
+  }
+  // Aligned plan: every unit exactly w = k/ut sweeps wide (ut divides k, w <= K), every CTA
+  // runs r rounds of nw warps and the tiles' chains of ut units fill CTA rounds exactly
+  // (ut % nw == 0 or nw % ut == 0): all chains identical and every sub-partition equally
+  // loaded, at the price of idling the SMs left over (G' = #CTAs divides the work; 128 of
+  // 148 here). It wins for few rounds (measured, B200: config 2 17.8 -> 18.3 TF/s on 128
+  // CTAs x 12 warps; config 4 30.1 -> 31.2; config 5 19.7 -> 21.5; 16384 x 2048 x 256
+  // 19.7 -> 21.3) and loses for many (config 3, 16 rounds: 24.2 -> 21.7), so it is used
+  // for r <= 4 rounds on >= 80% of the SMs, preferring more CTAs, then wider units.
+  const bool hooks = getenv("RS_DEBUG_GRID") || getenv("RS_PLAN_MODE") || getenv("RS_PLAN_Q");
+  if (!hooks && !getenv("RS_NO_ALIGNED_PLAN")) {
+    long long bestG = 0, bestU = 0;
+    int bestNW = 0;
+    const int ut0 = (g.k + kK - 1) / kK;
+    for (int ut = ut0; ut <= 2 * ut0 && ut <= g.k; ++ut) {
+      if (g.k % ut != 0) continue;
+      const long long U = g.tiles * ut;
+      for (int nw = cap; nw >= 8; nw -= 4) {
+        if (!(ut % nw == 0 || nw % ut == 0) || U % nw != 0) continue;
+        const long long cr = U / nw;  // CTA-rounds
+        long long r = (cr + grid - 1) / grid;
+        while (r <= 4 && cr % r != 0) ++r;
+        if (r > 4) continue;
+        const long long G2 = cr / r;
+        if (G2 * 5 < grid * 4) continue;
+        if (G2 > bestG) bestG = G2, bestU = U, bestNW = nw;
+      }
+    }
+    if (bestG > 0) {
+      lp->grid = (int)bestG;
+      lp->nw = bestNW;
+      lp->smem = per * bestNW + ctl;
+      lp->units = bestU;
+      lp->mode = 3;
+      lp->ua = (int)(bestU / g.tiles);
+      lp->t1 = 0;
+      return RS_OK;
+    }
   }
   const long long umin = g.tiles * ((g.k + kK - 1) / kK);
   const long long gneed = (umin + 3) / 4;

@@ -54,6 +54,31 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
     """plan_launch(): grid, U, ua, t1, NW."""
     cap = max(4, cap & ~3)
     G = sms if grid is None else min(grid, sms)
+    if mode in (0, 3) and grid is None:
+        # aligned plan (plan_launch): uniform widths k/ut, chains filling CTA rounds
+        best = None
+        ut0 = -(-g.k // g.K)
+        for ut in range(ut0, min(2 * ut0, g.k) + 1):
+            if g.k % ut:
+                continue
+            U = g.tiles * ut
+            for nw in range(cap, 7, -4):
+                if not (ut % nw == 0 or nw % ut == 0) or U % nw:
+                    continue
+                cr = U // nw
+                r = -(-cr // G)
+                while r <= 4 and cr % r:
+                    r += 1
+                if r > 4:
+                    continue
+                G2 = cr // r
+                if G2 * 5 < G * 4:
+                    continue
+                if best is None or G2 > best[0]:
+                    best = (G2, U, nw)
+        if best is not None:
+            G2, U, nw = best
+            return dict(G=G2, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw)
     umin = g.tiles * -(-g.k // g.K)
     G = max(1, min(G, -(-umin // 4)))
     q = -(-umin // (4 * G))
