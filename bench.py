@@ -356,7 +356,8 @@ def main():
         bo = hA.numel() * hA.element_size()
         e2e = {"value": flops_total / (float(t.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
-               "ms_per_step": float(t.item()), "api": "apply_cuda(pinned host torch tensors) -> rs_apply_host_* (chunked copy-in/compute/copy-out overlap)"}
+               "ms_per_step": float(t.item()),
+               "step_ms": {"min": min(e2e_ms), "median": statistics.median(e2e_ms), "max": max(e2e_ms)}, "api": "apply_cuda(pinned host torch tensors) -> rs_apply_host_* (chunked copy-in/compute/copy-out overlap)"}
 
     # roofline: the pipeline kernel against the live FMA-pipe peak
     peak = _lib.fma_peak_tflops(_lib.DTYPE_F64 if tdtype == torch.float64 else _lib.DTYPE_F32)

@@ -43,6 +43,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <type_traits>
 
@@ -82,9 +83,45 @@ struct Geometry {
   size_t flags_only = 0;    // progress flags (zeroed per launch)
   size_t flag_bytes = 0;    // flags + unsafe word + trash slot
   bool left = false;
+  bool streaming = false;  // host streaming (rs_apply_host_*): input-bound, plain plans only
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Library-private stream-ordered pool per device: scratch (workspace, device copies of
+// host matrices) is returned to it at the end of each call and reused by the next one
+// instead of being unmapped at every synchronisation (release threshold 2 GiB; the default
+// pool's threshold of 0 made every rs_apply_host_* call map ~150 MB afresh).
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev < 64 && pools[dev] == nullptr) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      cudaMemPool_t np = nullptr;
+      if (cudaMemPoolCreate(&np, &props) == cudaSuccess) {
+        uint64_t thr = 2ull << 30;
+        cudaMemPoolSetAttribute(np, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = np;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (dev < 64) pool = pools[dev];
+  }
+  if (pool == nullptr) return cudaMallocAsync(p, bytes, st);
+  return cudaMallocFromPoolAsync(p, bytes, pool, st);
+}
+
 
 bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int kind, int dtype, Geometry* g) {
   const bool left = side == RS_SIDE_LEFT;
@@ -163,7 +200,8 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   // 19.7 -> 21.3) and loses for many (config 3, 16 rounds: 24.2 -> 21.7), so it is used
   // for r <= 4 rounds on >= 80% of the SMs, preferring more CTAs, then wider units.
   const bool hooks = getenv("RS_DEBUG_GRID") || getenv("RS_PLAN_MODE") || getenv("RS_PLAN_Q");
-  if (!hooks && !getenv("RS_NO_ALIGNED_PLAN")) {
+  // (host streaming is input-bound: it keeps every SM, measured 3.61 vs 3.75 ms at config 2)
+  if (!hooks && !g.streaming && !getenv("RS_NO_ALIGNED_PLAN")) {
     long long bestG = 0, bestU = 0;
     int bestNW = 0;
     const int ut0 = (g.k + kK - 1) / kK;
@@ -459,7 +497,7 @@ rs_status apply_impl(int algo, T* A, int64_t m, int64_t n, int64_t lda, const T*
   void* ws = workspace;
   bool owned = false;
   if (ws == nullptr) {
-    cudaError_t e = cudaMallocAsync(&ws, need, st);
+    cudaError_t e = pool_alloc(&ws, need, st);
     if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("workspace allocation: ") + cudaGetErrorString(e));
     owned = true;
   } else if (ws_bytes < need) {
@@ -572,6 +610,7 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   if (!ops.ok) return fail(RS_EUNSUPPORTED, "stream memory operations unavailable");
   Geometry g;  // device copy of A is dense: ld = m
   make_geometry(m, n, m > 1 ? m : 1, k, side, kind, dtype, &g);
+  g.streaming = true;
   const int rev = order == RS_ORDER_REVERSE;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int dev = 0;
@@ -647,7 +686,7 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   unsigned char* mem = nullptr;
   const size_t off_c = align_up(abytes, 256), off_s = off_c + align_up(csbytes, 256);
   const size_t off_ws = off_s + align_up(csbytes, 256), off_ctl = off_ws + align_up(wsbytes, 256);  // = total
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&mem), off_ctl, st);
+  cudaError_t e = pool_alloc(reinterpret_cast<void**>(&mem), off_ctl, st);
   if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("device buffers: ") + cudaGetErrorString(e));
   T* dA = reinterpret_cast<T*>(mem);
   T* dC = reinterpret_cast<T*>(mem + off_c);
