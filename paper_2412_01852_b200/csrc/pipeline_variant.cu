@@ -13,7 +13,7 @@ namespace rsk {
 
 template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) {
-  auto kern = rs_pipeline_kernel<T, kK, kR, STRICT, REFL, HS, LEFT>;
+  auto kern = rs_pipeline_kernel<T, kK, rows_for(sizeof(T)), STRICT, REFL, HS, LEFT>;
   static std::atomic<int> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);

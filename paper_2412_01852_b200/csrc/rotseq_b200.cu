@@ -131,7 +131,8 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   g->os = left ? lda : 1;
   g->cs = left ? 1 : lda;
   g->k = (int)k;
-  g->tiles = (g->owners + kTileOwners - 1) / kTileOwners;
+  const int towners = tile_owners(dtype == RS_DTYPE_F64 ? 8 : 4);
+  g->tiles = (g->owners + towners - 1) / towners;
   g->pairs = g->tiles * g->k;
   g->nchunk = (g->len + kK) / (kK + 1);
   g->nblk = g->nchunk + 1;
@@ -160,7 +161,7 @@ size_t smem_per_warp(size_t tsz, size_t coef_rec) {
   size_t cbuf = (size_t)(kK + 1) * kK * coef_rec;  // == coef_buf_bytes<T, REFL>()
   const size_t scl = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
   if (scl > cbuf) cbuf = scl;
-  return 2 * cbuf + (size_t)stages_for(tsz) * (kK + 1) * kTileOwners * tsz + ctl_words(stages_for(tsz)) * sizeof(uint64_t);
+  return 2 * cbuf + (size_t)stages_for(tsz) * (kK + 1) * tile_owners(tsz) * tsz + ctl_words(stages_for(tsz)) * sizeof(uint64_t);
 }
 
 // Grid of G <= #SMs persistent CTAs and U = 4*G*q units (q per SM sub-partition, each
@@ -177,7 +178,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   // one extra control block: the (never dereferenced) out-ring words of the last warp
   const size_t ctl = ctl_words(stages_for(tsz)) * sizeof(uint64_t);
   int cap = (int)((optin - ctl) / per);
-  const int wmax = g.left ? kMaxWarpsLeft : kMaxWarps;
+  const int wmax = max_warps_for(tsz, g.left);
   if (cap > wmax) cap = wmax;
   cap &= ~3;
   if (cap < 4) return fail(RS_EUNSUPPORTED, "shared memory too small for one warp per sub-partition");
@@ -910,7 +911,7 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
   if (warps_per_cta) *warps_per_cta = lp.nw;
   if (units) *units = lp.units;
   if (band_width) *band_width = kK;
-  if (rows_per_tile) *rows_per_tile = kTileOwners;
+  if (rows_per_tile) *rows_per_tile = tile_owners(dtype == RS_DTYPE_F64 ? 8 : 4);
   if (smem_bytes) *smem_bytes = lp.smem;
   return RS_OK;
 }
