@@ -27,7 +27,10 @@ constexpr int kK = 8;          // max sweeps per unit (lanes of the wavefront)
 #ifndef RS_ROWS_F32
 #define RS_ROWS_F32 2
 #endif
-__host__ __device__ constexpr int rows_for(size_t tsz) { return tsz == 4 ? RS_ROWS_F32 : 2; }
+#ifndef RS_ROWS_F64
+#define RS_ROWS_F64 2
+#endif
+__host__ __device__ constexpr int rows_for(size_t tsz) { return tsz == 4 ? RS_ROWS_F32 : RS_ROWS_F64; }
 constexpr int kRMax = 4;
 #ifndef RS_FLAG_EVERY
 #define RS_FLAG_EVERY 8

@@ -117,3 +117,27 @@ def test_full_size_subset_parity_and_invariants(cuda, oracle_mod, cfg):
     whole = np.concatenate(parts, axis=1 if w.side.value == "left" else 0)
     assert_bitwise(strict, np.asfortranarray(whole), f"config {cfg} shard invariance")
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("m,n,k,side,dtype", [
+    (512, 512, 64, 0, 0), (4096, 4096, 192, 0, 0), (65536, 2048, 256, 0, 0), (8192, 8192, 128, 0, 1),
+    (16384, 16384, 96, 1, 0), (8192, 2048, 256, 0, 0), (16384, 2048, 256, 0, 0), (32768, 2048, 256, 0, 0),
+])
+def test_launch_plan_matches_schedule_model(cuda, m, n, k, side, dtype):
+    """plan_launch (C++) and the schedule model whose hand-off protocol the CPU suite
+    simulates for deadlock freedom (tests/pipeline_model.py) pick the same launch: grid,
+    warps per CTA and unit count, including the aligned plans."""
+    import torch
+
+    from paper_2412_01852_b200 import _lib
+    from pipeline_model import Geometry, plan, warp_cap
+
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("model parameters are for a 148-SM B200")
+    left = side == 1
+    tsz = 8 if dtype == 0 else 4
+    cap = warp_cap(tsz, S=3 if tsz == 4 else 2, max_warps=12 if left else 16)
+    owners, length = (n, m) if left else (m, n)
+    pl = plan(Geometry(owners=owners, length=length, k=k), cap=cap)
+    info = _lib.plan_info(m, n, k, side=side, dtype=dtype)
+    assert (info["grid_ctas"], info["warps_per_cta"], info["units"]) == (pl["G"], pl["NW"], pl["U"])
