@@ -103,42 +103,8 @@ template <typename T, bool REFL>
 constexpr bool kPairRecs = sizeof(T) == 4 && !REFL;
 __host__ __device__ constexpr int recs_per_wave(int kb, bool pair) { return pair ? (kb + 1) / 2 : kb; }
 // the (c, s) of lane l from a wave's records
-// 16-byte record load from shared memory as a volatile asm: keeps the loads where the
-// unrolled body issues them (a few rotation steps ahead of their use) instead of letting
-// the compiler sink them next to the FMAs that consume them
-template <typename CoefT>
-__device__ __forceinline__ CoefT lds_rec(const CoefT* p) {
-  static_assert(sizeof(CoefT) == 16, "16-byte records");
-  CoefT r;
-  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-  if constexpr (sizeof(r.c) == 8) {
-    double x, y;
-    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
-    memcpy(&r, &x, 8);
-    memcpy(reinterpret_cast<char*>(&r) + 8, &y, 8);
-  } else {
-    float x, y, z, w;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a));
-    float v[4] = {x, y, z, w};
-    memcpy(&r, v, 16);
-  }
-  return r;
-}
 template <bool PAIR, typename CoefT>
 __device__ __forceinline__ CoefT lane_coef(const CoefT* __restrict__ wrec, int l) {
-#ifdef RS_ASM_COEF
-  if constexpr (PAIR) {
-    const CoefT r = lds_rec(wrec + (l >> 1));
-    CoefT o = r;
-    if (l & 1) {
-      o.c = r.pad0;
-      o.s = r.pad1;
-    }
-    return o;
-  } else {
-    return lds_rec(wrec + l);
-  }
-#endif
   if constexpr (PAIR) {
     const CoefT r = wrec[l >> 1];
     CoefT o = r;
@@ -239,15 +205,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-#ifdef RS_X_SLEEP
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_test(bar, parity)) __nanosleep(RS_X_SLEEP);
-}
-#else
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-#ifndef RS_X_NOFASTWAIT
   if (mbar_test(bar, parity)) return;  // already complete: skip try_wait's fixed latency
-#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "RS_WAIT_%=:\n\t"
@@ -256,7 +215,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "r"(kSuspendHintNs)
       : "memory");
 }
-#endif
 // Address-based forms (shared-window u32 addresses computed once per warp) and single-lane
 // forms predicated inside the asm, so the per-block protocol has no divergent branches.
 __device__ __forceinline__ bool mbar_test_a(uint32_t bar, uint32_t parity) {
@@ -271,9 +229,7 @@ __device__ __forceinline__ bool mbar_test_a(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
-#ifndef RS_X_NOTEST
   if (mbar_test_a(bar, parity)) return;
-#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "RS_WAITA_%=:\n\t"
@@ -295,11 +251,7 @@ __device__ __forceinline__ void mbar_arrive_if(uint32_t bar, bool pred) {
 __device__ __forceinline__ void st_shared_u32_if(uint32_t a, uint32_t v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
-#ifdef RS_X_RELCONS
-      "@p st.release.cta.shared::cta.u32 [%0], %1;\n}" ::"r"(a),
-#else
       "@p st.volatile.shared::cta.u32 [%0], %1;\n}" ::"r"(a),
-#endif
       "r"(v), "r"((uint32_t)pred)
       : "memory");
 }
@@ -351,11 +303,7 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release_shared(uint32_t* p, uint32_t v) {
-#ifdef RS_X_RELAXED_CONSUMED
-  asm volatile("st.volatile.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-#else
   asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-#endif
 }
 __device__ __forceinline__ uint32_t ld_acquire_shared(const uint32_t* p) {
   uint32_t v;
@@ -466,25 +414,10 @@ struct Unit {
   int p0;  // first sweep
   int kb;  // sweeps (1..kK)
 };
-// First sweep of unit i (of ut) of a tile: the k sweeps split evenly, except that with
-// RS_X_HEAD=h (percent) the chain's head unit (i = 0) gets h% of the average width.
+// First sweep of unit i (of ut) of a tile: the k sweeps split evenly. (Uneven splits —
+// a narrower head unit, widths tapered along the chain — measured much slower: a chain
+// runs at the pace of its widest unit.)
 __host__ __device__ __forceinline__ int sweep_start(long long i, int ut, int k) {
-#ifdef RS_X_HEAD
-  if (ut > 1) {
-    int hw = (int)((long long)k * RS_X_HEAD / (100LL * ut));
-    if (hw < 1) hw = 1;
-    if ((long long)(k - hw) > (long long)(ut - 1) * kK) return (int)(i * k / ut);
-    if (i == 0) return 0;
-    return hw + (int)((i - 1) * (k - hw) / (ut - 1));
-  }
-#endif
-#ifdef RS_X_TAPER
-  // widths taper linearly along the chain: head (1 + a) x average, tail (1 - a) x average
-  if (ut > 1 && (double)k / ut * (1.0 + fabs(RS_X_TAPER / 100.0)) <= kK - 0.5) {
-    const double x = (double)i / ut, a = RS_X_TAPER / 100.0;
-    return (int)floor(k * (x + a * x * (1.0 - x)) + 0.5);
-  }
-#endif
   return (int)(i * k / ut);
 }
 __host__ __device__ __forceinline__ long long tile_first_unit(long long t, long long t1, int ua) {
@@ -546,14 +479,6 @@ __host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, lon
 //   or to A (global) through one generic store path, so a unit width compiles to ONE loop
 //   body (instruction-cache footprint). EDGE blocks check every column and lane at run time.
 // ------------------------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ void st_shared(uint32_t a, T v) {
-  if constexpr (sizeof(T) == 8) {
-    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"((double)v) : "memory");
-  } else {
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"((float)v) : "memory");
-  }
-}
 // OUTS: the output columns go to shared memory (the next unit's ring, or the left side's
 // staging slot) at obase + u*OSU + r*OSR elements and are stored with STS; otherwise to A
 // through the generic pointers op[r] (stride ostr[r]).
@@ -617,11 +542,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
           if constexpr (OUTS) {
             obase[u * OSU + r * OSR] = v;
           } else {
-#ifndef RS_X_NOGSTORE
             *q[r] = v;
-#else
-            if (v == T(1.2345e-300)) *q[r] = v;
-#endif
           }
         }
       }
@@ -679,11 +600,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 
   const int NW = P.nw;
   // warp-uniform for the compiler (uniform registers for the per-block protocol operands)
-#ifdef RS_X_NOSHFL
-  const int warp = threadIdx.x >> 5;
-#else
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
-#endif
   const int lane = threadIdx.x & 31;
   const bool lane0 = lane == 0;
   T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
@@ -769,16 +686,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     // The buffer's previous readers are this warp's own LDS, whose values were consumed
     // before the warp barrier that precedes every issue (no proxy fence needed for WAR).
     auto issue_coef = [&](int b, uint32_t buf) {
-#ifdef RS_X_OLDCOEF
-      if (lane == 0) {
-        uint64_t* bar = &cbar[buf];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, blk_bytes);
-        bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
-      }
-#else
       coef_copy_if(cbuf_a + buf * (uint32_t)CBUF, ubase + (size_t)b * brec, blk_bytes, cbar_a + buf * 8u, lane0);
-#endif
     };
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
     const uint32_t* myflag = P.flags + tile * k + p0;
@@ -978,17 +886,6 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       unsigned long long t5 = trace_clock();
       // LEFT global output: the last block stages in the slot of chunk nchunk-1, so that
       // slot is released one block later (as nchunk, i.e. iseq of the last block)
-#ifdef RS_X_OLDPOST
-      if (lane == 0) {
-        if (LEFT && !outring) {
-          if (has_in && b + 1 < nchunk) st_release_shared(consumed_in, iseq + 1u);
-          if (b == nchunk) st_release_shared(consumed_in, iseq);
-        } else if (has_in) {
-          st_release_shared(consumed_in, iseq + 1u);
-        }
-        if (outring && has_out) mbar_arrive(&full_out[ob]);
-      }
-#else
       if (LEFT && !outring) {
         if (has_in && b + 1 < nchunk) st_shared_u32_if(consin_a, iseq + 1u, lane0);
         if (b == nchunk) st_shared_u32_if(consin_a, iseq, lane0);
@@ -996,7 +893,6 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
         st_shared_u32_if(consin_a, iseq + 1u, lane0);
       }
       if (outring && has_out) mbar_arrive_if(fullout_a + ob * 8u, lane0);
-#endif
       if (dst == DST_FLAG && has_out &&
           (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b >= nblk - RS_FLAG_TAIL)) {
         if (lane0) {
@@ -1161,9 +1057,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     auto issue_coef = [&](int b, uint32_t buf) {
       if (lane == 0) {
         uint64_t* bar = &cbar[buf];
-#ifndef RS_X_NOPROXYFENCE
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
         mbar_expect_tx(bar, blk_bytes);
         bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
       }
