@@ -383,3 +383,21 @@ def test_host_streaming_pinned_tensors_and_fp32(cuda, oracle_mod):
     apply_host(A32, (seq.C.astype(np.float32), seq.S.astype(np.float32)), fast=True)
     ref32 = oracle_mod.upcast_reference(A0.astype(np.float32), seq.C.astype(np.float32), seq.S.astype(np.float32))
     assert np.linalg.norm(A32 - ref32) / np.linalg.norm(ref32) <= 10 * k * np.finfo(np.float32).eps
+
+
+def test_cli_run_and_verify(cuda, tmp_path):
+    """``python -m paper_2412_01852_b200.cli``: run writes the reference's CSV (and the
+    extended columns with the kernel's peak fraction) and verifies small cases against
+    cuda-naive; verify runs the criterion-1 grid bit for bit."""
+    from paper_2412_01852_b200 import cli
+
+    out = tmp_path / "run.csv"
+    assert cli.main(["run", "--algo", "cuda", "--n", "96", "--m", "70", "--k", "9", "--reps", "2",
+                     "--csv", str(out), "--csv-extended", "--strict-arith", "on"]) == 0
+    lines = out.read_text().splitlines()
+    assert lines[0] == "n,Flops,algo,m,k,threads,reps,seconds,verified,kernel_seconds,peak_frac"
+    assert lines[1].split(",")[8] == "True"
+    out2 = tmp_path / "sweep.csv"
+    assert cli.main(["run", "--sweep", "64", "128", "--k", "12", "--reps", "1", "--csv", str(out2)]) == 0
+    assert out2.read_text().splitlines()[0] == "n,Flops" and len(out2.read_text().splitlines()) == 3
+    assert cli.main(["verify", "--quick"]) == 0

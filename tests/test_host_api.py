@@ -154,3 +154,14 @@ def test_enums_accept_strings():
     A, seq = make_inputs(0, 4, 1, 0)
     apply_cuda(A, seq, kind="reflector", side="right", order="reverse")
     assert TransformKind("rotation") is TransformKind.ROTATION
+
+
+def test_cli_argument_errors_exit_2(capsys):
+    """rotbench-compatible CLI: a ValueError (here: run without --n) exits 2 before any
+    GPU work, as the reference CLI does (cli.py:372-374); argparse rejects bad choices."""
+    from paper_2412_01852_b200 import cli
+
+    assert cli.main(["run", "--algo", "cuda"]) == 2
+    assert "needs --n" in capsys.readouterr().err
+    with pytest.raises(SystemExit):
+        cli.main(["run", "--algo", "kernel", "--n", "8"])
