@@ -94,6 +94,9 @@ struct alignas(4 * sizeof(T)) Coef<T, true> {
 template <typename T>
 using SCoef = Coef<T, false>;
 constexpr int kScaleRecs = 5;  // per block: K+1 = 9 column scales (fp64) in 5 16-byte records
+// blocks per coefficient buffer: the right side copies them in pairs; the left side (whose
+// global chunk copies go through L1, which shares the SRAM with shared memory) one by one
+__host__ __device__ constexpr int coef_blocks_per_buf(bool left) { return left ? 1 : 2; }
 
 // fp32 rotation records (standard and scaled) hold two lanes each; everything else one.
 // A unit of width kb then stores recs_per_wave(kb) records per wave; units keep the
@@ -603,7 +606,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const bool lane0 = lane == 0;
-  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
+  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * coef_blocks_per_buf(LEFT) * CBUF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
 
   T* const A = reinterpret_cast<T*>(P.A);
@@ -622,7 +625,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
-  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
+  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * coef_blocks_per_buf(LEFT) * CBUF;
   // shared-window addresses of this warp's protocol words and buffers
   const uint32_t fullin_a = smem_u32(full_in), fullout_a = smem_u32(full_out);
   const uint32_t consin_a = smem_u32(consumed_in), cbar_a = smem_u32(cbar), cbuf_a = smem_u32(cbuf);
@@ -686,7 +689,8 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     // The buffer's previous readers are this warp's own LDS, whose values were consumed
     // before the warp barrier that precedes every issue (no proxy fence needed for WAR).
     auto issue_coef = [&](int b, uint32_t buf) {
-      coef_copy_if(cbuf_a + buf * (uint32_t)CBUF, ubase + (size_t)b * brec, blk_bytes, cbar_a + buf * 8u, lane0);
+      coef_copy_if(cbuf_a + buf * (uint32_t)(coef_blocks_per_buf(LEFT) * CBUF), ubase + (size_t)b * brec, blk_bytes, cbar_a + buf * 8u,
+                   lane0);
     };
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
     const uint32_t* myflag = P.flags + tile * k + p0;
@@ -848,7 +852,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 #endif
       unsigned long long t4 = trace_clock();
       {
-        const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + cbi * CBUF);
+        const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + cbi * coef_blocks_per_buf(LEFT) * CBUF);
         if (LEFT || outring) {
           run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, obase, b, len, Kb,
                                                                           lane, b < nchunk, b >= 1);
@@ -977,7 +981,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * CBUF);
+  T* ring_sm = reinterpret_cast<T*>(smem_raw + (size_t)NW * 2 * coef_blocks_per_buf(LEFT) * CBUF);
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring_sm + (size_t)NW * S * CHUNK);
 
   T* const A = reinterpret_cast<T*>(P.A);
@@ -996,11 +1000,11 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
-  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * CBUF;
+  unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * coef_blocks_per_buf(LEFT) * CBUF;
 
   const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
   const long long npos = cr.g1 - cr.g0;
-  uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
+  uint32_t cseq = 0;  // coefficient block pairs consumed by this warp (buffer = cseq&1)
 
   for (int jr = 0;; ++jr) {
     const long long pos = (long long)jr * NW + slot;
@@ -1054,12 +1058,15 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     }
     const uint32_t blk_bytes = (uint32_t)(brec * sizeof(CoefT));
     // one elected lane: WAR fence for the buffer's previous readers, arm, start the copy
+    // coefficient blocks travel in pairs (blocks 2i, 2i+1: one bulk copy, one wait per two
+    // blocks); pair i goes to buffer (cseq + i) & 1
     auto issue_coef = [&](int b, uint32_t buf) {
       if (lane == 0) {
         uint64_t* bar = &cbar[buf];
+        const uint32_t bytes = (b + 1 < nblk ? 2u : 1u) * blk_bytes;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(bar, blk_bytes);
-        bulk_g2s_nowait(cbuf + (size_t)buf * CBUF, ubase + (size_t)b * brec, blk_bytes, bar);
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s_nowait(cbuf + (size_t)buf * coef_blocks_per_buf(LEFT) * CBUF, ubase + (size_t)b * brec, bytes, bar);
       }
     };
     const uint32_t seq0 = (uint32_t)jr * (uint32_t)nchunk;
@@ -1170,11 +1177,8 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
       constexpr int KB = decltype(kb_c)::value;
       constexpr bool EDGE = decltype(edge_c)::value;
       unsigned long long t0 = trace_clock();
-#ifdef RS_X_NOCOEF
-      if (b + 1 < nblk && b < 1) issue_coef(b + 1, (cseq + 1) & 1);
-#else
-      if (b + 1 < nblk) issue_coef(b + 1, (cseq + 1) & 1);
-#endif
+      const bool pair_start = (b & 1) == 0;
+      if (pair_start && b + 2 < nblk) issue_coef(b + 2, (cseq + 1) & 1);
       const bool has_in = !EDGE || b < nchunk;
       const bool has_out = !EDGE || b >= 1;
       if (self && b + FA < nchunk) fill_chunk(b + FA);
@@ -1204,11 +1208,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 #pragma unroll
         for (int r = 0; r < R; ++r) op[r] = grow[r] + cb0 * gcs[r], ostr[r] = gcs[r];
       }
-#ifdef RS_X_NOCOEF
-      if (b < 2) mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
-#else
-      mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
-#endif
+      if (pair_start) mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
       unsigned long long t2 = trace_clock();
 #ifndef RS_X_NOSYNC
       if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
@@ -1220,7 +1220,8 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 #endif
       unsigned long long t4 = trace_clock();
       {
-        const CoefT* cbp = reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * CBUF);
+        const CoefT* cbp =
+            reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * coef_blocks_per_buf(LEFT) * CBUF + (b & 1) * blk_bytes);
         // ring output by STS (default) or through the generic store path shared with A
         // outputs (P.ring_sts = 0: one loop body per unit width)
         if (outring && P.ring_sts) {
@@ -1293,11 +1294,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
         __syncwarp();
         if (lane == 0) mbar_arrive(&full_in[(iseq + 1u) % S]);
       }
-#ifdef RS_X_NOCOEF
-      if (b < 2) ++cseq;
-#else
-      ++cseq;
-#endif
+      if ((b & 1) == 1 || b + 1 == nblk) ++cseq;
       unsigned long long t6 = trace_clock();
       tacc.c[0] += t1 - t0;
       tacc.c[1] += t2 - t1;
@@ -1337,7 +1334,8 @@ __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pip
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * CBUF + (size_t)NW * S * (K + 1) * 32 * R * sizeof(T));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * coef_blocks_per_buf(LEFT) * CBUF +
+                                               (size_t)NW * S * (K + 1) * 32 * R * sizeof(T));
   // "full" is alias-safe as an mbarrier (the consumer has always seen chunk seq-S before it
   // waits for seq); "consumed" is a monotonic counter because a ring's producer changes
   // between rounds (previous warp vs. self-fill), which a parity test cannot express.

@@ -42,11 +42,12 @@ class Geometry:
 
 
 def warp_cap(dtype_bytes: int = 8, refl: bool = False, R: int = 2, K: int = 8, S: int = 2,
-             optin: int = 232448, max_warps: int = 16) -> int:
-    """plan_launch()'s shared-memory bound on warps per CTA (a multiple of 4)."""
+             optin: int = 232448, max_warps: int = 16, left: bool = False) -> int:
+    """plan_launch()'s shared-memory bound on warps per CTA (a multiple of 4). The right
+    side's coefficient buffers hold block pairs (coef_blocks_per_buf)."""
     rec = (4 if refl else 2) * dtype_bytes
     cbuf = max((K + 1) * K * max(rec, 16), ((K + 1) * K + 5) * 16)
-    per = 2 * cbuf + S * (K + 1) * 32 * R * dtype_bytes + (S + 3) * 8
+    per = 2 * (1 if left else 2) * cbuf + S * (K + 1) * 32 * R * dtype_bytes + (S + 3) * 8
     return min(max_warps, (optin - (S + 3) * 8) // per) & ~3
 
 
