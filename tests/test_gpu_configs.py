@@ -136,7 +136,7 @@ def test_launch_plan_matches_schedule_model(cuda, m, n, k, side, dtype):
         pytest.skip("model parameters are for a 148-SM B200")
     left = side == 1
     tsz = 8 if dtype == 0 else 4
-    cap = warp_cap(tsz, S=3 if tsz == 4 else 2, max_warps=12 if left else 16, left=left)
+    cap = warp_cap(tsz, S=2, max_warps=12 if left else 16, left=left)
     owners, length = (n, m) if left else (m, n)
     pl = plan(Geometry(owners=owners, length=length, k=k), cap=cap)
     info = _lib.plan_info(m, n, k, side=side, dtype=dtype)
