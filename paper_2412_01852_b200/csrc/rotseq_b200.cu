@@ -161,7 +161,7 @@ size_t smem_per_warp(size_t tsz, size_t coef_rec, bool left) {
   size_t cbuf = (size_t)(kK + 1) * kK * coef_rec;  // == coef_buf_bytes<T, REFL>()
   const size_t scl = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
   if (scl > cbuf) cbuf = scl;
-  return 2 * coef_blocks_per_buf(left) * cbuf + (size_t)stages_for(tsz) * (kK + 1) * tile_owners(tsz) * tsz + ctl_words(stages_for(tsz)) * sizeof(uint64_t);
+  return 2 * coef_blocks_per_buf(left) * cbuf + (size_t)stages_for(tsz) * (kK + 1) * tile_owners(tsz) * tsz + ctl_words(stages_for(tsz), left) * sizeof(uint64_t);
 }
 
 // Grid of G <= #SMs persistent CTAs and U = 4*G*q units (q per SM sub-partition, each
@@ -176,7 +176,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
   const size_t per = smem_per_warp(tsz, g.coef_rec, g.left);
   // one extra control block: the (never dereferenced) out-ring words of the last warp
-  const size_t ctl = ctl_words(stages_for(tsz)) * sizeof(uint64_t);
+  const size_t ctl = ctl_words(stages_for(tsz), g.left) * sizeof(uint64_t);
   int cap = (int)((optin - ctl) / per);
   const int wmax = max_warps_for(tsz, g.left);
   if (cap > wmax) cap = wmax;

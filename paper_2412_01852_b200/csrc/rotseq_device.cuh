@@ -47,7 +47,16 @@ constexpr int kRMax = 4;
 // ring depth in chunks of K+1 columns (self-fill runs S-1 ahead). 3-chunk fp32 rings
 // measured 2.4% slower at config 4 (the larger shared-memory carve-out shrinks L1).
 __host__ __device__ constexpr int stages_for(size_t tsz) { return tsz == 4 ? RS_STAGES_F32 : RS_STAGES; }
-__host__ __device__ constexpr int ctl_words(int stages) { return stages + 3; }  // per-warp control words
+// Right-side rings can hand chunks over in kSub sub-chunks of (K+1)/kSub columns (the
+// consumer starts a block once its first columns are in): one "full" barrier per
+// (slot, sub-chunk). RS_SUBCHUNK=1 enables it (default off: 1 sub-chunk).
+#ifndef RS_SUBCHUNK
+#define RS_SUBCHUNK 0
+#endif
+constexpr int kSub = RS_SUBCHUNK ? 3 : 1;
+__host__ __device__ constexpr int full_bars(int stages, bool left) { return left ? stages : stages * kSub; }
+// per-warp control words: full barriers, the consumed counter, two coefficient barriers
+__host__ __device__ constexpr int ctl_words(int stages, bool left) { return full_bars(stages, left) + 3; }
 #ifndef RS_RIGHT_LEAN
 #define RS_RIGHT_LEAN 0
 #endif
@@ -490,7 +499,11 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* islot, T* const (&op)[R], const long long (&ostr)[R],
                                           T* obase, int b, int len, int Kb, int lane, bool has_in_rt,
-                                          bool has_out_rt) {
+                                          bool has_out_rt, uint64_t* sub_in = nullptr, uint32_t sub_par = 0,
+                                          uint64_t* sub_out = nullptr) {
+  // sub-chunk hand-off (kSub > 1, right side): wait for sub-chunk h before loading its first
+  // column; announce sub-chunk h once its last column is stored
+  constexpr int SUBW = (K + 1) / kSub;
   // OUTS: element strides of the output column (u) and row (r) in the shared slot
   constexpr int OSU = LEFT ? 1 : 32 * R;
   constexpr int OSR = LEFT ? 32 * (K + 1) : 32;
@@ -534,6 +547,9 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
     T nv[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) nv[r] = nxt[r];
+    if constexpr (kSub > 1) {
+      if (u < K && (u + 1) % SUBW == 0 && sub_in != nullptr) mbar_wait(&sub_in[(u + 1) / SUBW], sub_par);
+    }
     if (u < K) load_col(u + 1, nxt);
     // outgoing column (LEFT may stage it in place of the column just read)
     if (has_out) {
@@ -552,6 +568,12 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
       if constexpr (!OUTS) {
 #pragma unroll
         for (int r = 0; r < R; ++r) q[r] += ostr[r];
+      }
+      if constexpr (kSub > 1) {
+        if (u % SUBW == SUBW - 1 && sub_out != nullptr) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sub_out[u / SUBW]);
+        }
       }
     }
 #pragma unroll
@@ -599,7 +621,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   constexpr int S = stages_for(sizeof(T));
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
-  constexpr int NBAR = ctl_words(S);
+  constexpr int NBAR = ctl_words(S, LEFT);
 
   const int NW = P.nw;
   // warp-uniform for the compiler (uniform registers for the per-block protocol operands)
@@ -976,7 +998,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   constexpr int S = stages_for(sizeof(T));
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
-  constexpr int NBAR = ctl_words(S);
+  constexpr int NBAR = ctl_words(S, LEFT);
 
   const int NW = P.nw;
   const int warp = threadIdx.x >> 5;
@@ -990,14 +1012,17 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   const int nchunk = P.nchunk;
   const int nblk = P.nblk;
   const uint32_t credit = (uint32_t)P.credit;
-  uint64_t* const bar_in = bars + warp * NBAR;  // in-ring of this warp: full[S], consumed, coef[2]
+  constexpr int FB = full_bars(S, false);
+  constexpr int SUB = kSub;
+  // in-ring of this warp: full[S][SUB], consumed, coef[2]
+  uint64_t* const bar_in = bars + warp * NBAR;
   uint64_t* const full_in = bar_in;
-  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + S);
-  uint64_t* const cbar = bar_in + S + 1;
+  uint32_t* const consumed_in = reinterpret_cast<uint32_t*>(bar_in + FB);
+  uint64_t* const cbar = bar_in + FB + 1;
   // position p of a round runs on warp p % NW; the next position on warp + 1
   const int slot = warp;
   uint64_t* const full_out = bars + (warp + 1) * NBAR;
-  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + S);
+  const uint32_t* const consumed_out = reinterpret_cast<const uint32_t*>(full_out + FB);
   T* const rin = ring_sm + (size_t)warp * S * CHUNK;
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
   unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * coef_blocks_per_buf(LEFT) * CBUF;
@@ -1159,7 +1184,9 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
       else
         cp_async_wait_group<0>();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_in[seq0 % S]);
+      if (lane == 0)
+#pragma unroll
+        for (int h = 0; h < SUB; ++h) mbar_arrive(&full_in[(seq0 % S) * SUB + h]);
     }
     tacc.c[0] += trace_clock() - tc;
 
@@ -1211,7 +1238,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
       if (pair_start) mbar_wait(&cbar[cseq & 1], (cseq >> 1) & 1u);
       unsigned long long t2 = trace_clock();
 #ifndef RS_X_NOSYNC
-      if (!self && has_in) mbar_wait(&full_in[iseq % S], (iseq / S) & 1u);
+      if (!self && has_in) mbar_wait(&full_in[(iseq % S) * SUB], (iseq / S) & 1u);
 #endif
       unsigned long long t3 = trace_clock();
       // ring credit: the producer runs at most `credit` chunks ahead of its consumer
@@ -1224,12 +1251,17 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
             reinterpret_cast<const CoefT*>(cbuf + (cseq & 1) * coef_blocks_per_buf(LEFT) * CBUF + (b & 1) * blk_bytes);
         // ring output by STS (default) or through the generic store path shared with A
         // outputs (P.ring_sts = 0: one loop body per unit width)
+        uint64_t* const sub_in = (SUB > 1 && !self && has_in) ? &full_in[(iseq % S) * SUB] : nullptr;
+        uint64_t* const sub_out = (SUB > 1 && outring && has_out) ? &full_out[(oseq % S) * SUB] : nullptr;
+        const uint32_t sub_par = (iseq / S) & 1u;
         if (outring && P.ring_sts) {
           run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, op[0], b, len, Kb,
-                                                                          lane, b < nchunk, b >= 1);
+                                                                          lane, b < nchunk, b >= 1, sub_in, sub_par,
+                                                                          sub_out);
         } else {
           run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, nullptr, b, len,
-                                                                           Kb, lane, b < nchunk, b >= 1);
+                                                                           Kb, lane, b < nchunk, b >= 1, sub_in,
+                                                                           sub_par, sub_out);
         }
       }
       __syncwarp();
@@ -1268,7 +1300,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
         } else if (has_in) {
           st_release_shared(consumed_in, iseq + 1u);
         }
-        if (outring && has_out) mbar_arrive(&full_out[oseq % S]);
+        if (SUB == 1 && outring && has_out) mbar_arrive(&full_out[oseq % S]);
         if (dst == DST_FLAG && has_out &&
             (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b >= nblk - RS_FLAG_TAIL)) {
           // the warp barrier above orders every lane's stores before lane 0's gpu-scope
@@ -1292,7 +1324,9 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
         else
           cp_async_wait_group<0>();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&full_in[(iseq + 1u) % S]);
+        if (lane == 0)
+#pragma unroll
+          for (int h = 0; h < SUB; ++h) mbar_arrive(&full_in[((iseq + 1u) % S) * SUB + h]);
       }
       if ((b & 1) == 1 || b + 1 == nblk) ++cseq;
       unsigned long long t6 = trace_clock();
@@ -1330,7 +1364,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
 __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
   constexpr int S = stages_for(sizeof(T));
-  constexpr int NBAR = ctl_words(S);
+  constexpr int NBAR = ctl_words(S, LEFT);
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
@@ -1341,11 +1375,12 @@ __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pip
   // between rounds (previous warp vs. self-fill), which a parity test cannot express.
   if (threadIdx.x < NW) {
     uint64_t* bw = bars + threadIdx.x * NBAR;
+    constexpr int FB = full_bars(S, LEFT);
 #pragma unroll
-    for (int i = 0; i < S; ++i) mbar_init(bw + i, 1);
-    *reinterpret_cast<volatile uint32_t*>(bw + S) = 0u;
-    mbar_init(bw + S + 1, 1);
-    mbar_init(bw + S + 2, 1);
+    for (int i = 0; i < FB; ++i) mbar_init(bw + i, 1);
+    *reinterpret_cast<volatile uint32_t*>(bw + FB) = 0u;
+    mbar_init(bw + FB + 1, 1);
+    mbar_init(bw + FB + 2, 1);
   }
   __syncthreads();
   // fast mode: the scaled form, unless the pack found coefficients outside its safe range
