@@ -291,7 +291,10 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   int bx = (per_p + 255) / 256;
   if (bx > 64) bx = 64;
   const int rows = nparts * g.k;
-  const int by = rows < 65535 ? rows : 65535;
+  // rows are grid-strided: a capped grid keeps the (usual) early exit after the scaled
+  // pack cheap (3264 CTAs that only test the unsafe word cost ~4 us at config 2); up to
+  // 64 x 32 CTAs of 256 threads still saturate HBM when the standard records are written
+  const int by = rows < 32 ? rows : 32;
   // Scaled records first (fast mode); the standard records are the fallback the pipeline
   // uses when the scaled form is out of range, so a per-call pack (std_only_if_unsafe)
   // lets the standard pack kernel exit at once when the scaled records are safe. The
