@@ -1529,18 +1529,33 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
         if (j + 1 <= len - 2) coef(j + 1, p0 + l, cr[l], sd);
       }
     }
-    double sa = 1, sb = 1;  // running scales of columns j and j+1
+    // running scales of columns j and j+1 (a short multiply chain), then the taus of all
+    // kb rotations independently (their divisions overlap)
+    double sal[kK], sbl[kK];
+    double sa = 1, sb = 1;
     bool bad = false;
 #pragma unroll
     for (int l = 0; l < kK; ++l) {
-      if (l >= kb) break;
-      if (j >= 1) sa *= REFL ? -cl[l] : cl[l];  // rotation (j-1, p) touched column j as its y
-      if (j <= len - 2) {
+      if (l < kb) {
+        if (j >= 1) sa *= REFL ? -cl[l] : cl[l];  // rotation (j-1, p) touched column j as its y
+        sal[l] = sa;
+        sbl[l] = sb;
+        if (j <= len - 2) {
+          sa *= cj[l];
+          sb *= REFL ? -cj[l] : cj[l];
+          if (j + 1 <= len - 2) sb *= cr[l];  // rotation (j+1, p) touches column j+1 as its x
+        }
+        bad |= !(fabs(sa) >= lo && fabs(sa) <= hi) || !(fabs(sb) >= lo && fabs(sb) <= hi);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < kK; ++l) {
+      if (l < kb && j <= len - 2) {
         const double c = cj[l], s = sj[l];
         // tau1 = s*sb / (c*sa), tau2 = s*sa / (c*sb), with one division
-        const double q = 1.0 / (c * sa * sb);
-        const double t1 = s * sb * sb * q;
-        const double t2 = s * sa * sa * q;
+        const double q = 1.0 / (c * sal[l] * sbl[l]);
+        const double t1 = s * sbl[l] * sbl[l] * q;
+        const double t2 = s * sal[l] * sal[l] * q;
         bad |= !(c != 0.0) || !(fabs(t1) <= hi) || !(fabs(t2) <= hi);
         // rotation (j, p) runs in block b at wave u with b(K+1) + u = j + 1 + l
         const int bu = j + 1 + l;
@@ -1555,11 +1570,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
         } else {
           ubase[(size_t)b * brec + u * kb + l] = rec;
         }
-        sa *= c;
-        sb *= REFL ? -c : c;
-        if (j + 1 <= len - 2) sb *= cr[l];  // rotation (j+1, p) touches column j+1 as its x
       }
-      bad |= !(fabs(sa) >= lo && fabs(sa) <= hi) || !(fabs(sb) >= lo && fabs(sb) <= hi);
     }
     // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
     const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
