@@ -141,3 +141,27 @@ def test_launch_plan_matches_schedule_model(cuda, m, n, k, side, dtype):
     pl = plan(Geometry(owners=owners, length=length, k=k), cap=cap)
     info = _lib.plan_info(m, n, k, side=side, dtype=dtype)
     assert (info["grid_ctas"], info["warps_per_cta"], info["units"]) == (pl["G"], pl["NW"], pl["U"])
+
+
+@pytest.mark.parametrize("m,n,k,side", [
+    (16384, 2048, 256, "right"),  # aligned plan, 4 rounds per CTA
+    (8192, 2048, 256, "right"),   # aligned plan, 2 rounds
+    (2048, 8192, 96, "left"),     # left side, aligned plan (one chain per CTA round)
+])
+def test_aligned_plans_bitwise_vs_naive_kernel(cuda, m, n, k, side):
+    """Aligned launch plans (uniform unit widths, chains filling CTA rounds) in strict
+    arithmetic equal the independent one-thread-per-owner GPU kernel bit for bit."""
+    import torch
+
+    from paper_2412_01852_b200 import apply_device
+
+    g = torch.Generator(device="cpu").manual_seed(11)
+    A = torch.randn(n, m, dtype=torch.float64, generator=g).to(cuda).t()  # column-major m x n
+    ln = m if side == "left" else n
+    th = torch.rand(k, ln - 1, dtype=torch.float64, generator=g).t() * 6.283185307179586
+    C, S = torch.cos(th).to(cuda), torch.sin(th).to(cuda)
+    B = A.clone(memory_format=torch.preserve_format)
+    apply_device(A, (C, S), fast=False, side=side)
+    apply_device(B, (C, S), fast=False, side=side, algo="naive")
+    torch.cuda.synchronize()
+    assert_bitwise(B.cpu().numpy(), A.cpu().numpy())
