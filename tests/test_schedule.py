@@ -139,3 +139,27 @@ def test_kernel_emulator_golden(golden):
         A = golden[f"c{i}_A"]
         got = emulate(A, golden[f"c{i}_C"], golden[f"c{i}_S"])
         assert_bitwise(golden[f"c{i}_rot_right_fwd"], got)
+
+
+@pytest.mark.parametrize("owners,length,k,cap,expect", [
+    (4096, 4096, 192, 16, dict(G=128, NW=12, U=1536)),     # config 2: 2 CTAs per tile chain
+    (8192, 8192, 128, 16, dict(G=128, NW=16, U=2048)),     # config 4: 1 CTA per chain
+    (16384, 16384, 96, 12, dict(G=128, NW=12, U=3072)),    # config 5: 2 rounds, 1 chain each
+    (65536, 2048, 256, 16, dict(G=148, NW=16, U=32768)),   # config 3: many rounds keep all SMs
+])
+def test_aligned_plans_for_baseline_configs(owners, length, k, cap, expect):
+    """The planner picks uniform-width, chain-aligned plans for the few-round BASELINE
+    configs and keeps every SM for the many-round config 3."""
+    g = Geometry(owners=owners, length=length, k=k)
+    pl = plan(g, cap=cap)
+    assert {key: pl[key] for key in expect} == expect
+    if pl["G"] == 128:
+        assert pl["t1"] == 0 and k % pl["ua"] == 0  # every unit exactly k/ut sweeps wide
+
+
+@pytest.mark.parametrize("owners,length,k,cap", [(16384, 16384, 96, 12), (16384, 2048, 256, 16)])
+def test_protocol_deadlock_free_on_multi_round_aligned_plans(owners, length, k, cap):
+    """Config 5 on one GPU (2 rounds, one chain per round) and the 4-GPU shard of config 3
+    (4 rounds): the aligned plans' ring and flag hand-offs complete in the simulation."""
+    res = simulate(Geometry(owners=owners, length=length, k=k), cap=cap)
+    assert res["plan"]["G"] == 128
