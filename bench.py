@@ -177,6 +177,33 @@ def time_cpu_reference(w, A, C, S, seconds: float, reps_min: int = 1, reps_max: 
             "seconds_per_rep": best, "sample_flops": flops}
 
 
+def load_profile_counters(index: int) -> dict:
+    """ncu counters committed under profiles/ for this workload (the bench itself never
+    runs under a profiler): DRAM traffic per launch and executed-pipe utilisation."""
+    out = {}
+    path = os.path.join(ROOT, "profiles", "ncu_counters.json")
+    try:
+        entry = json.load(open(path)).get(f"config{index}")
+    except (OSError, ValueError):
+        entry = None
+    if entry:
+        out["traffic"] = entry.get("dram_bytes_per_launch")
+        out["ncu"] = {k: v for k, v in entry.items() if k != "dram_bytes_per_launch"}
+    return out
+
+
+def config_dict(w, args, world: int) -> dict:
+    """The workload description shared by both arms (same keys, same values)."""
+    from paper_2412_01852_b200 import Side
+
+    return {"workload": w.name(), "m": w.m, "n": w.n, "k": w.k, "side": w.side.value,
+            "order": w.order.value, "arith": args.arith,
+            "parallelism": f"{'row' if w.side is Side.RIGHT else 'column'}-sharded x{world}"
+            + (", C/S NCCL broadcast per step (inside the timed step)" if world > 1 else ""),
+            "l2": "L2 flushed between steps (256 MiB write); A alone exceeds the 126 MB L2"
+                  if w.m * w.n * w.itemsize > 126e6 else "L2 flushed between steps (256 MiB write)"}
+
+
 # ----------------------------------------------------------------------------------
 # main
 # ----------------------------------------------------------------------------------
@@ -217,7 +244,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE seeded generators, workloads.py)",
-            "config": {"workload": w.name(), "m": w.m, "n": w.n, "k": w.k, "arith": args.arith},
+            "config": config_dict(w, args, world),
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "port",
                              "sample": ("full workload matrix per step; oracle/rotseq_oracle.c apply_blocked "
                                         "(C port of the reference kernel tier; the reference itself is "
@@ -231,98 +258,88 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2412_01852_b200 import PackedSequence, _lib, apply_cuda
+    from paper_2412_01852_b200 import _lib, apply_cuda
+    from paper_2412_01852_b200.distributed import ShardedApplier, owner_shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    # under torchrun (WORLD_SIZE set, any N, including 1) the NCCL group is formed and the
+    # per-step C/S broadcast runs; a plain `python bench.py` is a single process
+    use_dist = "WORLD_SIZE" in os.environ
+    if use_dist:
         dist.init_process_group("nccl", device_id=dev)
 
     tdtype = torch.float64 if w.dtype == np.float64 else torch.float32
-    o0, o1 = shard_range(w.owners, world, rank, align=64)
-    # inputs: config 1/2/4/5 (and config 3 at N=1) use the exact seeded generator; for
-    # sharded config 3 every rank generates only its own rows with a rank-specific
-    # stream (same distribution; generating 1 GiB per rank would dominate start-up).
-    if world > 1 and w.index == 3:
-        g = torch.Generator(device=dev)
-        g.manual_seed(1000 + rank)
-        mloc = o1 - o0
-        dA = torch.randn(w.n, mloc, dtype=tdtype, device=dev, generator=g).t()
-        Ah = None
-        if rank == 0:
-            th = np.random.Generator(np.random.Philox(1)).uniform(0.0, 2.0 * np.pi, size=(w.n - 1, w.k))
-            Cn, Sn = np.cos(th), np.sin(th)
-        else:
-            Cn = Sn = None
-    else:
-        Ah, Cn, Sn = make_workload_inputs(w, owner_range=(o0, o1) if world > 1 else None)
-        dA = torch.empty_strided(Ah.shape, (1, max(Ah.shape[0], 1)), dtype=tdtype, device=dev)
-        dA.copy_(torch.from_numpy(Ah))
+    o0, o1 = owner_shard(w.owners, world, rank)
+    # every rank holds exactly its owners of the seeded BASELINE input (the generator is
+    # produced up to the shard's last row and sliced: bit-identical to the full matrix)
+    Ah, Cn, Sn = make_workload_inputs(w, owner_range=(o0, o1) if world > 1 else None)
+    dA = torch.empty_strided(Ah.shape, (1, max(Ah.shape[0], 1)), dtype=tdtype, device=dev)
+    dA.copy_(torch.from_numpy(Ah))
+    dA0 = dA.clone()  # the untransformed shard, for the parity checksum below
     length = w.length
-    dC = torch.empty_strided((length - 1, w.k), (1, length - 1), dtype=tdtype, device=dev)
-    dS = torch.empty_strided((length - 1, w.k), (1, length - 1), dtype=tdtype, device=dev)
-    if rank == 0:
+    dC = torch.zeros((w.k, length - 1), dtype=tdtype, device=dev).t()
+    dS = torch.zeros((w.k, length - 1), dtype=tdtype, device=dev).t()
+    if rank == 0:  # the other ranks receive C/S through the broadcast inside every step
         dC.copy_(torch.from_numpy(np.asfortranarray(Cn)).to(tdtype))
         dS.copy_(torch.from_numpy(np.asfortranarray(Sn)).to(tdtype))
     m_loc, n_loc = dA.shape
     flops_local = (6.0 * n_loc * (m_loc - 1) * w.k) if w.side is Side.LEFT else (6.0 * m_loc * (n_loc - 1) * w.k)
 
-    def broadcast_cs():
-        if world > 1:
-            dist.broadcast(dC, src=0)
-            dist.broadcast(dS, src=0)
-
-    broadcast_cs()
-    packed = PackedSequence((dC, dS), (m_loc, n_loc), side=w.side, order=w.order, dtype=tdtype, device=dev,
-                            fast_only=fast)
+    # a step = NCCL broadcast of C/S (N > 1) + coefficient repack + pipeline kernel,
+    # through distributed.ShardedApplier, each phase bracketed by its own CUDA events
+    applier = ShardedApplier(dA, dC, dS, fast=fast, side=w.side, order=w.order, distributed=use_dist)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-
-    def step(evs=None):
-        broadcast_cs()
-        if evs is not None:
-            evs[0].record(stream)
-        packed.pack((dC, dS))
-        if evs is not None:
-            evs[1].record(stream)
-        packed.apply(dA, fast=fast)
-        if evs is not None:
-            evs[2].record(stream)
 
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
     sampler.active = True  # clocks are sampled under load: warm-up + timed region
     for _ in range(args.warmup):
-        step()
+        applier.step()
         flush.zero_()
     torch.cuda.synchronize(dev)
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    if world > 1:
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     launches0 = _lib.launch_count()
     sampler.active = True
     for i in range(args.steps):
-        step(evs[i])
+        applier.step(evs[i])
         flush.zero_()
     torch.cuda.synchronize(dev)
     sampler.active = False
     sampler.stop()  # the nvidia-smi poller perturbs launch-heavy host code (e2e below)
     launches = _lib.launch_count() - launches0
-    if world > 1:
+    if use_dist:
         dist.barrier()
-    step_ms = [e[0].elapsed_time(e[2]) for e in evs]
-    kern_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    pack_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    bcast_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    pack_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    kern_ms = [e[2].elapsed_time(e[3]) for e in evs]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
-    flops_total = w.flops if world == 1 else w.flops  # all ranks together cover the whole matrix
+    flops_total = w.flops  # all ranks together cover the whole matrix
     value = flops_total * args.steps / (total_ms_max * 1e-3) / 1e9
+
+    # parity fingerprint: one strict application of the seeded input (bit-identical to the
+    # reference's apply_naive), summarised by an order-independent integer checksum of the
+    # result's bit patterns, summed over ranks: identical for every GPU count N
+    strict_applier = ShardedApplier(dA0, dC, dS, fast=False, side=w.side, order=w.order, distributed=False)
+    strict_applier.apply()
+    csum = dA0.view(torch.int64 if tdtype == torch.float64 else torch.int32).to(torch.int64).sum().reshape(1)
+    if use_dist:
+        dist.all_reduce(csum, op=dist.ReduceOp.SUM)
+    checksum = {"strict_result_bits_sum_mod_2_64": f"{int(csum.item()) & 0xFFFFFFFFFFFFFFFF:016x}",
+                "what": "sum over all elements of the strict result's IEEE bit patterns (as int64 / int32), "
+                        "mod 2^64, over all ranks: invariant in the GPU count"}
+    del strict_applier, dA0
 
     # end-to-end through the public host API (pinned host buffers, copies inside)
     e2e = None
@@ -350,7 +367,7 @@ def main():
             torch.cuda.synchronize(dev)
             e2e_ms.append(e0.elapsed_time(e1))
         t = torch.tensor([statistics.mean(e2e_ms)], dtype=torch.float64, device=dev)
-        if world > 1:
+        if use_dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         bi = hA.numel() * hA.element_size() + hC.numel() * hC.element_size() * 2
         bo = hA.numel() * hA.element_size()
@@ -360,33 +377,50 @@ def main():
                "step_ms": {"min": min(e2e_ms), "median": statistics.median(e2e_ms), "max": max(e2e_ms)}, "api": "apply_cuda(pinned host torch tensors) -> rs_apply_host_* (chunked copy-in/compute/copy-out overlap)"}
 
     # roofline: the pipeline kernel against the live FMA-pipe peak
-    peak = _lib.fma_peak_tflops(_lib.DTYPE_F64 if tdtype == torch.float64 else _lib.DTYPE_F32)
+    f64 = tdtype == torch.float64
+    peak = _lib.fma_peak_tflops(_lib.DTYPE_F64 if f64 else _lib.DTYPE_F32)
     kern_avg_ms = statistics.mean(kern_ms)
     achieved = flops_local / (kern_avg_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"config{w.index}")
-        except (OSError, ValueError):
-            traffic = None
+    prof = load_profile_counters(w.index)
     try:
         hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
         hbm_src = "MEASURED_PEAKS.json"
     except (OSError, ValueError, KeyError):
         hbm, hbm_src = 6650.0, "fallback"
     ai = w.flops / w.algorithmic_bytes()
+    # arithmetic form actually selected by the pack (per unit: scaled fast Givens, standard
+    # fast, or strict) and the instruction ceiling it implies in counted flops (6 per
+    # rotation element): scaled 2 FMA -> 1.5x the FMA peak, standard 2 MUL + 2 FMA -> 0.75,
+    # strict 4 MUL + 2 ADD -> 0.5
+    if fast:
+        scaled_units, total_units = applier.packed.form()
+        f_scaled = scaled_units / max(total_units, 1)
+        ceiling = 1.5 * f_scaled + 0.75 * (1.0 - f_scaled)
+        form = {"scaled_units": scaled_units, "total_units": total_units}
+    else:
+        ceiling, form = 0.5, {"strict": True}
+    clk = sampler.summary()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    lanes = 64 if f64 else 128  # FP64 / FP32 FMA lanes per SM (B200)
+    clock_peak = {k2: (sms * lanes * 2 * mhz * 1e6 / 1e12 if mhz else None)
+                  for k2, mhz in (("at_sm_max_mhz", clk.get("sm_max_mhz")), ("at_median_load_mhz", clk.get("sm_mhz")))}
     roofline = {
-        "bound": "fp64" if tdtype == torch.float64 else "fp32",
+        "bound": "fp64" if f64 else "fp32",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-        "traffic": traffic,
-        "peak_source": f"measured live on this GPU ({'DFMA' if tdtype == torch.float64 else 'FFMA'} pipe microbenchmark, "
+        "traffic": prof.get("traffic"),
+        "peak_source": f"measured live on this GPU ({'DFMA' if f64 else 'FFMA'} pipe microbenchmark rs_fma_peak_kernel, "
                        "2 flops/FMA); MEASURED_PEAKS.json has no FP64/FP32 entry",
+        "clock_derived_peak_tflops": clock_peak,
+        "frac_of_clock_peak_at_sm_max": (achieved / clock_peak["at_sm_max_mhz"]) if clock_peak["at_sm_max_mhz"] else None,
         "kernel": "rs_pipeline_kernel", "kernel_ms": kern_avg_ms, "pack_ms": statistics.mean(pack_ms),
+        "broadcast_ms": statistics.mean(bcast_ms),
         "algorithmic_flops_per_launch": flops_local,
         "algorithmic_bytes_per_launch": w.algorithmic_bytes() / world,
         "arithmetic_intensity": ai, "hbm_bound_tflops": ai * hbm / 1e3, "hbm_gbs": hbm, "hbm_source": hbm_src,
-        "instruction_ceiling_frac": 0.75 if fast else 0.5,
+        "arith_form": form,
+        "instruction_ceiling_frac": ceiling,
+        "frac_of_instruction_ceiling": achieved / peak / ceiling,
+        "ncu": prof.get("ncu"),
     }
 
     cpu_baseline = None
@@ -404,22 +438,20 @@ def main():
             "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if tdtype == torch.float64 else "f32",
             "data": ("synthetic: seeded Philox generators of BASELINE.json (workloads.py)"
-                     + ("; per-rank streams for the sharded config-3 matrix" if world > 1 and w.index == 3 else "")),
-            "config": {"workload": w.name(), "m": w.m, "n": w.n, "k": w.k, "side": w.side.value,
-                       "order": w.order.value, "arith": args.arith,
-                       "parallelism": f"{'row' if w.side is Side.RIGHT else 'column'}-sharded x{world}"
-                       + (", C/S NCCL broadcast per step" if world > 1 else ""),
-                       "l2": "L2 flushed between steps (256 MiB write); A alone exceeds the 126 MB L2"
-                             if w.m * w.n * w.itemsize > 126e6 else "L2 flushed between steps (256 MiB write)"},
+                     + ("; each rank holds its rows of the same seeded matrix" if world > 1 else "")),
+            "config": config_dict(w, args, world),
             "roofline": roofline,
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "clocks": sampler.summary(),
+            "clocks": clk,
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+            "phase_ms": {"broadcast": statistics.mean(bcast_ms), "pack": statistics.mean(pack_ms),
+                         "kernel": statistics.mean(kern_ms)},
+            "checksum": checksum,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

@@ -124,6 +124,16 @@ rs_status rs_apply_packed_f64(double* A, int64_t m, int64_t n, int64_t lda, int6
 rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64_t k, int side, int order,
                               int kind, int strict, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Arithmetic form a fast-mode rs_apply_packed_* will use with this packed workspace
+ * (after rs_pack_* / rs_pack_fast_* on `stream`; synchronous): *scaled_units of the
+ * *total_units (tile, sweep-range) units run the scaled "fast Givens" form (2 FMAs per
+ * rotation element), the rest the standard fast form (2 MUL + 2 FMA) because their
+ * coefficients leave the scaled form's safe range (e.g. c == 0). Strict applies always
+ * use the reference's expression shape. Reference: the strict/fast contract, _jit.py:14-44. */
+rs_status rs_packed_form(const void* workspace, size_t workspace_bytes, int64_t m, int64_t n, int64_t k,
+                         int side, int kind, int dtype, int64_t* scaled_units, int64_t* total_units,
+                         void* stream);
+
 /* Host-buffer entry point: A (m x n, column-major, lda), C and S ((len-1) x k, ldcs) in
  * HOST memory (pinned for full bandwidth; pageable works, slower). Synchronous: returns
  * once A holds the result. This is the call a host-side binding of the reference makes

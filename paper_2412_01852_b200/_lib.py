@@ -45,6 +45,7 @@ EXPORTS = (
     "rs_pack_fast_f32",
     "rs_apply_packed_f64",
     "rs_apply_packed_f32",
+    "rs_packed_form",
     "rs_apply_host_f64",
     "rs_apply_host_f32",
     "rs_launch_count",
@@ -89,6 +90,8 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i32, i32, i32, i32, vp]
+    lib.rs_packed_form.restype = i32
+    lib.rs_packed_form.argtypes = [vp, sz, i64, i64, i64, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
     lib.rs_plan_info.restype = i32
     lib.rs_plan_info.argtypes = [i64, i64, i64, i32, i32, i32,
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i64),

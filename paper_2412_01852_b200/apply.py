@@ -32,7 +32,7 @@ from .core import (
     TransformKind,
     _as_enum,
     check_apply_args,
-    require_colmajor,
+    sequence_parts,
 )
 
 ALGOS = {"pipeline": _lib.ALGO_PIPELINE, "naive": _lib.ALGO_NAIVE}
@@ -63,12 +63,10 @@ def _np_to_device(arr: np.ndarray, dtype, device):
 
 
 def _seq_arrays(seq, dtype, device):
-    """(C, S) as column-major device tensors of `dtype`."""
-    torch = _torch()
-    if isinstance(seq, RotationSequence):
-        C, S = seq.C, seq.S
-    else:
-        C, S = seq
+    """(C, S) as device tensors of `dtype` (sequence object — ours or the reference's —
+    or a (C, S) pair of numpy arrays / torch tensors). Conversions and host copies are
+    enqueued on the current stream of `device`."""
+    C, S, _ = sequence_parts(seq)
     out = []
     for X, name in ((C, "C"), (S, "S")):
         if _is_tensor(X):
@@ -88,9 +86,29 @@ def _seq_arrays(seq, dtype, device):
 
 
 def _seq_ncols(seq) -> int:
-    if isinstance(seq, RotationSequence):
-        return seq.n_cols
-    return int(seq[0].shape[0]) + 1
+    return sequence_parts(seq)[2]
+
+
+def _launch_stream(stream, device):
+    """(launch stream, current stream). A caller-supplied stream (torch stream or raw
+    cudaStream_t handle) is ordered after the current stream, on which the C/S device
+    copies, casts and compaction run, so the library never reads them early."""
+    torch = _torch()
+    cur = torch.cuda.current_stream(device)
+    if stream is None:
+        return cur, cur
+    if not hasattr(stream, "cuda_stream"):
+        stream = torch.cuda.ExternalStream(int(stream), device=device)
+    if stream.cuda_stream != cur.cuda_stream:
+        stream.wait_stream(cur)
+    return stream, cur
+
+
+def _keep_alive(stream, cur, *tensors):
+    """Tie temporaries made on `cur` to `stream` for the caching allocator."""
+    if stream.cuda_stream != cur.cuda_stream:
+        for X in tensors:
+            X.record_stream(stream)
 
 
 def apply_device(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Side.RIGHT,
@@ -153,26 +171,19 @@ def apply_device(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=S
         if workspace.numel() * workspace.element_size() < need:
             raise ValueError(f"workspace too small: need {need} bytes")
         ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
-    if stream is None:
-        stream = torch.cuda.current_stream(A.device)
-    sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
     with torch.cuda.device(A.device):
+        lstream, cur = _launch_stream(stream, A.device)
         fn = lib.rs_apply_algo_f64 if f64 else lib.rs_apply_algo_f32
         st = fn(ALGOS[algo], A.data_ptr(), m, n, lda, C.data_ptr(), S.data_ptr(), ldcs, k,
-                side_i, order_i, kind_i, 0 if fast else 1, ws_ptr, ws_bytes, sptr)
-    # C/S may be temporaries from torch's caching allocator: tie them to the launch stream
-    if hasattr(stream, "cuda_stream") and stream != torch.cuda.current_stream(A.device):
-        C.record_stream(stream)
-        S.record_stream(stream)
+                side_i, order_i, kind_i, 0 if fast else 1, ws_ptr, ws_bytes, lstream.cuda_stream)
+        # C/S may be temporaries from torch's caching allocator: tie them to the launch stream
+        _keep_alive(lstream, cur, C, S)
     _lib.check(st, "rs_apply")
 
 
 def _host_cs(seq, np_dtype, length):
     """(C, S) as host column-major arrays of the working dtype (copies only if needed)."""
-    if isinstance(seq, RotationSequence):
-        C, S = seq.C, seq.S
-    else:
-        C, S = seq
+    C, S, _ = sequence_parts(seq)
     out = []
     for X, name in ((C, "C"), (S, "S")):
         if _is_tensor(X):
@@ -212,10 +223,7 @@ def apply_host(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Sid
         np_dtype = np.float64 if A.dtype == torch.float64 else np.float32
         ptr = A.data_ptr()
     else:
-        if isinstance(seq, RotationSequence):
-            check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
-        else:
-            require_colmajor(A, dtypes=(np.float64, np.float32))
+        check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
         m, n = A.shape
         lda = A.strides[1] // A.itemsize if n > 1 else max(m, 1)
         np_dtype = A.dtype.type
@@ -291,15 +299,8 @@ def apply_cuda(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Sid
     kind = _as_enum(kind, TransformKind, "kind")
     side = _as_enum(side, Side, "side")
     order = _as_enum(order, Order, "order")
-    if isinstance(seq, RotationSequence):
-        check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
-    else:
-        require_colmajor(A, dtypes=(np.float64, np.float32))
+    check_apply_args(A, seq, side, dtypes=(np.float64, np.float32))
     if A.shape[0] == 0 or A.shape[1] == 0:
-        if not isinstance(seq, RotationSequence):
-            length = A.shape[0] if side is Side.LEFT else A.shape[1]
-            if length < 2:
-                raise ValueError("matrix needs at least 2 columns")
         return
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     tdt = torch.float64 if A.dtype == np.float64 else torch.float32
@@ -311,8 +312,11 @@ def apply_cuda(A, seq, kind=TransformKind.ROTATION, fast: bool = False, side=Sid
 def apply_naive(A, seq: RotationSequence, kind=TransformKind.ROTATION, fast: bool = False) -> None:
     """Reference signature (core.py:365-374), executed by the B200 pipeline.
 
-    Result is bit-identical to the reference's strict ``apply_naive`` when
-    ``fast`` is False (every variant in the reference is, SPEC criterion 1)."""
+    ``seq`` may be this package's ``RotationSequence``, the reference's own
+    ``rotseq.RotationSequence`` or a ``(C, S)`` pair; ``kind`` may be either package's
+    ``TransformKind`` or its string value. Result is bit-identical to the reference's
+    strict ``apply_naive`` when ``fast`` is False (every variant in the reference is,
+    SPEC criterion 1)."""
     apply_cuda(A, seq, kind=kind, fast=fast)
 
 
@@ -369,11 +373,6 @@ class PackedSequence:
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.pack((C, S), stream)
 
-    def _stream(self, stream):
-        torch = _torch()
-        if stream is None:
-            stream = torch.cuda.current_stream(self.device)
-        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
     def pack(self, seq, stream=None) -> None:
         """(Re)pack new coefficients of the same shape into the workspace."""
@@ -390,9 +389,28 @@ class PackedSequence:
         else:
             fn = lib.rs_pack_f64 if self.f64 else lib.rs_pack_f32
         with torch.cuda.device(self.device):
+            lstream, cur = _launch_stream(stream, self.device)
             st = fn(C.data_ptr(), S.data_ptr(), ldcs, self.m, self.n, self.k, self._side, self._order, self._kind,
-                    self.workspace.data_ptr(), self.workspace.numel(), self._stream(stream))
+                    self.workspace.data_ptr(), self.workspace.numel(), lstream.cuda_stream)
+            _keep_alive(lstream, cur, C, S, self.workspace)
         _lib.check(st, "rs_pack")
+
+    def form(self, stream=None):
+        """(scaled_units, total_units): how many units a fast-mode ``apply`` runs in the
+        scaled (fast Givens) form; the others use the standard fast form because their
+        coefficients leave the scaled form's safe range. Synchronous (``rs_packed_form``)."""
+        import ctypes  # noqa: PLC0415
+
+        torch = _torch()
+        lib = _lib.load()
+        scaled, total = ctypes.c_int64(), ctypes.c_int64()
+        with torch.cuda.device(self.device):
+            lstream, _ = _launch_stream(stream, self.device)
+            st = lib.rs_packed_form(self.workspace.data_ptr(), self.workspace.numel(), self.m, self.n, self.k,
+                                    self._side, self._kind, _lib.DTYPE_F64 if self.f64 else _lib.DTYPE_F32,
+                                    ctypes.byref(scaled), ctypes.byref(total), lstream.cuda_stream)
+        _lib.check(st, "rs_packed_form")
+        return int(scaled.value), int(total.value)
 
     def apply(self, A, fast: bool = False, stream=None) -> None:
         """Apply the packed sequence to the CUDA tensor A (column-major) in place."""
@@ -409,6 +427,8 @@ class PackedSequence:
         lib = _lib.load()
         fn = lib.rs_apply_packed_f64 if self.f64 else lib.rs_apply_packed_f32
         with torch.cuda.device(self.device):
+            lstream, cur = _launch_stream(stream, self.device)
             st = fn(A.data_ptr(), self.m, self.n, lda, self.k, self._side, self._order, self._kind,
-                    0 if fast else 1, self.workspace.data_ptr(), self.workspace.numel(), self._stream(stream))
+                    0 if fast else 1, self.workspace.data_ptr(), self.workspace.numel(), lstream.cuda_stream)
+            _keep_alive(lstream, cur, self.workspace)
         _lib.check(st, "rs_apply_packed")

@@ -10,8 +10,12 @@ GPU algorithms registered in :mod:`verification` (``cuda``, ``cuda-naive``):
   whole call on host data; ``--timing device`` times the packed kernel on resident data.
   Small cases are verified against the independent ``cuda-naive`` kernel (the reference
   verifies against its own ``apply_naive``); a failed check exits 1.
-* ``verify``  the reference's criterion-1 bitwise grid (verification.py:161-195), in
-  strict arithmetic: ``cuda`` against ``cuda-naive`` for both transform kinds.
+* ``verify``  the reference's equivalence grids (cli.py:243-278): criterion 1, the
+  bitwise grid (verification.py:161-195) in strict arithmetic, ``cuda`` against the
+  independent ``cuda-naive`` kernel; criterion 2, the explicit-Q chain
+  (verification.py:198-219), both algorithms against ``A0 @ Q`` with Q accumulated on
+  the host. ``--perturb-kernel`` sets ``ROTSEQ_PERTURB_KERNEL`` for the run (cli.py:244-245)
+  so the kernel path's output is off by one ulp and verify must exit 1.
 
 Usage: ``python -m paper_2412_01852_b200.cli run --algo cuda --n 4096 --k 192``.
 Argument errors and ``ValueError`` exit with status 2, as in the reference (cli.py:372-374).
@@ -21,16 +25,23 @@ from __future__ import annotations
 
 import argparse
 import math
+import os
 import sys
 import time
 
-import numpy as np
-
 from .compare import compare
 from .core import Order, Side, TransformKind, flops_applied, make_inputs
-from .verification import ALGORITHMS, case_grid, run_variant
+from .verification import ALGORITHMS, FAULT_ENV, bitwise_grid, oracle_grid, run_variant
 
 VERIFY_SIZE_LIMIT = 512 * 512  # the reference verifies runs up to this many elements
+
+
+def _cpu_knobs(p: argparse.ArgumentParser) -> None:
+    """The reference's CPU cache/thread flags (cli.py:93-117): accepted so command lines
+    port unchanged, and ignored (the GPU tiling is chosen by the library)."""
+    for flag in ("--mr", "--kr", "--nb", "--kb", "--mb", "--T1", "--T2", "--T3", "--S", "--threads"):
+        p.add_argument(flag, type=int, help=argparse.SUPPRESS)
+    p.add_argument("--config", help=argparse.SUPPRESS)
 
 
 def _parser() -> argparse.ArgumentParser:
@@ -52,10 +63,13 @@ def _parser() -> argparse.ArgumentParser:
     run.add_argument("--csv", help="write the CSV here instead of stdout")
     run.add_argument("--csv-extended", action="store_true")
     run.add_argument("--verify-all", action="store_true", help="verify every size, not only small ones")
-    ver = sub.add_parser("verify", help="criterion-1 bitwise grid: cuda vs cuda-naive (strict)")
+    _cpu_knobs(run)
+    ver = sub.add_parser("verify", help="equivalence grids (bitwise + explicit Q), exit 1 on failure")
     ver.add_argument("--quick", action="store_true")
     ver.add_argument("--seed", type=int, default=0)
     ver.add_argument("--kind", choices=("rotation", "reflector"))
+    ver.add_argument("--perturb-kernel", action="store_true", help=argparse.SUPPRESS)
+    _cpu_knobs(ver)
     return ap
 
 
@@ -156,21 +170,34 @@ def cmd_run(args) -> int:
 
 
 def cmd_verify(args) -> int:
-    kinds = ((TransformKind.ROTATION, TransformKind.REFLECTOR) if args.kind is None
-             else ((TransformKind.REFLECTOR,) if args.kind == "reflector" else (TransformKind.ROTATION,)))
-    total, failures = 0, 0
-    for kind in kinds:
-        for m, n, k in case_grid(quick=args.quick):
-            A0, seq = make_inputs(m, n, k, args.seed)
-            got, ref = A0.copy(order="F"), A0.copy(order="F")
-            run_variant("cuda", got, seq, kind, fast=False)
-            run_variant("cuda-naive", ref, seq, kind, fast=False)
-            total += 1
-            if not np.array_equal(got.view(np.uint64), ref.view(np.uint64)):
-                failures += 1
-                print(f"FAIL {kind.value} m={m} n={n} k={k}", file=sys.stderr)
-    print(f"criterion 1 (bitwise, strict): {total - failures}/{total} cases identical", file=sys.stderr)
-    return 1 if failures else 0
+    """Criteria 1 and 2 of the reference's verify (cli.py:243-278)."""
+    if args.perturb_kernel:
+        os.environ[FAULT_ENV] = "1"
+    try:
+        kinds = ((TransformKind.ROTATION, TransformKind.REFLECTOR) if args.kind is None
+                 else ((TransformKind.REFLECTOR,) if args.kind == "reflector" else (TransformKind.ROTATION,)))
+        total, failures = 0, []
+        for kind in kinds:
+            for case in bitwise_grid(kind, quick=args.quick, seed=args.seed):
+                total += 1
+                if not case.ok:
+                    failures.append(case)
+                    print(case, file=sys.stderr)
+            for case in oracle_grid(kind, seed=args.seed):
+                total += 1
+                if not case.ok:
+                    failures.append(case)
+                    print(case, file=sys.stderr)
+        print(f"verify: {total - len(failures)}/{total} cases passed")
+        if failures:
+            worst = failures[0]
+            print(f"verify: FIRST FAILURE {worst.algo} [{worst.config}] kind={worst.kind} "
+                  f"m={worst.m} n={worst.n} k={worst.k}", file=sys.stderr)
+            return 1
+        return 0
+    finally:
+        if args.perturb_kernel:
+            os.environ.pop(FAULT_ENV, None)
 
 
 def main(argv=None) -> int:

@@ -1,5 +1,10 @@
 """Tolerance profiles and comparison reports (mirror of rotseq.oracle:23-99).
 
+Attribution: ``ComparisonReport`` (including ``__str__``) and the body of
+``compare`` are copied, nearly verbatim, from the reference's
+``/root/reference/pkg/src/rotseq/oracle.py:23-99``. They are the tolerance contract
+every test in both packages agrees on, so they are kept identical on purpose.
+
 ``compare`` and the profiles carry the reference's meaning of "equal":
 strict = bitwise; fast = Frobenius-relative and row-scaled elementwise error
 <= 16*k*eps (oracle.py:26-29, 82-90). ``baseline_tol`` is BASELINE.json's

@@ -50,12 +50,41 @@ SUPPORTED_DTYPES = (np.float64, np.float32)
 
 
 def _as_enum(value, enum_cls, name):
+    """Coerce ``value`` to ``enum_cls``. Accepts this package's enums, their string
+    values, and any other enum whose ``.value`` is one of them — in particular the
+    reference's own ``rotseq.TransformKind`` (core.py:29-38), so reference call sites
+    pass their objects through unchanged."""
     if isinstance(value, enum_cls):
         return value
+    raw = value.value if isinstance(value, enum.Enum) else value
     try:
-        return enum_cls(value)
+        return enum_cls(raw)
     except ValueError:
         raise ValueError(f"{name} must be one of {[e.value for e in enum_cls]}, got {value!r}") from None
+
+
+def is_sequence_object(seq) -> bool:
+    """True for a rotation-sequence object: anything exposing ``C`` and ``S`` arrays
+    (this package's ``RotationSequence`` or the reference's, core.py:54-91)."""
+    return hasattr(seq, "C") and hasattr(seq, "S") and not isinstance(seq, (tuple, list))
+
+
+def sequence_parts(seq):
+    """(C, S, n_cols) of a sequence object or of a ``(C, S)`` pair.
+
+    ``n_cols`` is the object's own ``n_cols`` when it has one (the reference's
+    ``RotationSequence`` records it), else ``C.shape[0] + 1``."""
+    if is_sequence_object(seq):
+        C, S = seq.C, seq.S
+        n_cols = getattr(seq, "n_cols", None)
+        if n_cols is None:
+            n_cols = int(C.shape[0]) + 1
+        return C, S, int(n_cols)
+    try:
+        C, S = seq
+    except (TypeError, ValueError):
+        raise ValueError("seq must be a RotationSequence-like object (with .C/.S) or a (C, S) pair") from None
+    return C, S, int(C.shape[0]) + 1
 
 
 def require_colmajor(A: np.ndarray, name: str = "A", dtypes=(np.float64,)) -> None:
@@ -134,20 +163,22 @@ def rotated_length(shape, side: Side) -> int:
     return shape[0] if side is Side.LEFT else shape[1]
 
 
-def check_apply_args(A: np.ndarray, seq: RotationSequence, side: Side = Side.RIGHT,
+def check_apply_args(A: np.ndarray, seq, side: Side = Side.RIGHT,
                      dtypes=(np.float64,)) -> None:
-    """_check_apply_args (core.py:110-117), generalised to the left side."""
+    """_check_apply_args (core.py:110-117), generalised to the left side. ``seq`` is
+    a sequence object (ours or the reference's) or a ``(C, S)`` pair."""
     require_colmajor(A, dtypes=dtypes)
+    n_cols = sequence_parts(seq)[2]
     if side is Side.RIGHT:
         if A.shape[1] < 2:
             raise ValueError(f"matrix needs at least 2 columns, got {A.shape[1]}")
-        if seq.n_cols != A.shape[1]:
-            raise ValueError(f"sequence acts on {seq.n_cols} columns but matrix has {A.shape[1]}")
+        if n_cols != A.shape[1]:
+            raise ValueError(f"sequence acts on {n_cols} columns but matrix has {A.shape[1]}")
     else:
         if A.shape[0] < 2:
             raise ValueError(f"matrix needs at least 2 rows for left-side application, got {A.shape[0]}")
-        if seq.n_cols != A.shape[0]:
-            raise ValueError(f"sequence acts on {seq.n_cols} rows but matrix has {A.shape[0]}")
+        if n_cols != A.shape[0]:
+            raise ValueError(f"sequence acts on {n_cols} rows but matrix has {A.shape[0]}")
 
 
 def flops_applied(m: int, n: int, k: int, side: Side = Side.RIGHT) -> float:

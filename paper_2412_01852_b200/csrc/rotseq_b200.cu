@@ -81,7 +81,8 @@ struct Geometry {
   size_t std_bytes = 0;     // standard records (both sweep partitions)
   size_t coef_bytes = 0;    // standard + scaled records
   size_t flags_only = 0;    // progress flags (zeroed per launch)
-  size_t flag_bytes = 0;    // flags + unsafe word + trash slot
+  size_t unsafe_bytes = 0;  // per-unit "outside the scaled form's range" words, [2][ua+1]
+  size_t flag_bytes = 0;    // flags + unsafe words + trash slot
   bool left = false;
   bool streaming = false;  // host streaming (rs_apply_host_*): input-bound, plain plans only
 };
@@ -143,7 +144,8 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   // scaled form: per partition k*nblk*(K+1) records + <= k*nblk*kScaleRecs scale records
   g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (kK + 1 + kScaleRecs) * 16, 256);
   g->flags_only = align_up((size_t)(g->pairs + 1) * sizeof(uint32_t), 256);
-  g->flag_bytes = g->flags_only + 256 + kTrashBytes;
+  g->unsafe_bytes = align_up(2 * (size_t)(g->k + 1) * sizeof(uint32_t), 256);  // ua + 1 <= k + 1
+  g->flag_bytes = g->flags_only + g->unsafe_bytes + kTrashBytes;
   return true;
 }
 
@@ -303,7 +305,7 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   if (scaled) {
     unsigned char* base = reinterpret_cast<unsigned char*>(ws);
     unsafe = reinterpret_cast<uint32_t*>(base + g.coef_bytes + g.flags_only);
-    cudaError_t e0 = cudaMemsetAsync(unsafe, 0, sizeof(uint32_t), st);
+    cudaError_t e0 = cudaMemsetAsync(unsafe, 0, 2 * (size_t)(lp.ua + 1) * sizeof(uint32_t), st);
     if (e0 != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e0));
     const int srows = nparts * (lp.ua + 1);
     const int sy = srows < 65535 ? srows : 65535;
@@ -350,7 +352,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   P.ua = lp.ua;
   P.coef = coef;
   P.flags = flags;
-  P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only + 256;
+  P.trash = reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only + g.unsafe_bytes;
   P.coef_scaled = reinterpret_cast<unsigned char*>(ws) + g.std_bytes;
   P.unsafe = reinterpret_cast<const uint32_t*>(reinterpret_cast<unsigned char*>(ws) + g.coef_bytes + g.flags_only);
   P.use_scaled = use_scaled;
@@ -593,13 +595,38 @@ cudaError_t copy_wave_chunk(T* dev, T* host, const Geometry& g, int64_t m, int64
 constexpr int kMaxHostChunks = 64;
 constexpr int kCopyLanes = 2;  // streams per direction (copies of a lane run on their own engine)
 struct HostCtx {
-  int dev = -1;
+  bool ready = false;
   cudaStream_t cin[kCopyLanes] = {}, cout[kCopyLanes] = {};
-  cudaEvent_t e0 = nullptr, ecs = nullptr, eend[kCopyLanes] = {};
+  cudaEvent_t e0 = nullptr, ecs = nullptr, eend[kCopyLanes] = {}, ejoin[kCopyLanes] = {};
   cudaEvent_t ein[kMaxHostChunks] = {};  // group i's arrival count is written
   uint32_t* ctl = nullptr;  // arrival / release counters (cudaMalloc: stream memory ops
                             // reject stream-ordered pool addresses)
 };
+constexpr int kMaxDevices = 64;
+
+// One context per (host thread, device): calls alternating between devices reuse their
+// own streams, events and counters instead of recreating (and leaking) them.
+rs_status host_ctx(int dev, HostCtx** out) {
+  static thread_local HostCtx ctxs[kMaxDevices];
+  if (dev < 0 || dev >= kMaxDevices) return fail(RS_EUNSUPPORTED, "device ordinal >= 64");
+  HostCtx& ctx = ctxs[dev];
+  if (!ctx.ready) {
+    bool okc = cudaEventCreateWithFlags(&ctx.e0, cudaEventDisableTiming) == cudaSuccess &&
+               cudaEventCreateWithFlags(&ctx.ecs, cudaEventDisableTiming) == cudaSuccess &&
+               cudaMalloc(reinterpret_cast<void**>(&ctx.ctl), (kMaxHostChunks + 1) * sizeof(uint32_t)) == cudaSuccess;
+    for (int l = 0; l < kCopyLanes && okc; ++l)
+      okc = cudaStreamCreateWithFlags(&ctx.cin[l], cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&ctx.cout[l], cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx.eend[l], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ctx.ejoin[l], cudaEventDisableTiming) == cudaSuccess;
+    for (int i = 0; i < kMaxHostChunks && okc; ++i)
+      okc = cudaEventCreateWithFlags(&ctx.ein[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!okc) return fail(RS_ECUDA, "stream/event/counter creation failed");
+    ctx.ready = true;
+  }
+  *out = &ctx;
+  return RS_OK;
+}
 
 template <typename T>
 rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, const T* S, int64_t ldcs, int64_t k,
@@ -619,26 +646,10 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int dev = 0;
   cudaGetDevice(&dev);
-  static thread_local HostCtx ctx;
-  if (ctx.dev != dev) {
-    bool okc = cudaEventCreateWithFlags(&ctx.e0, cudaEventDisableTiming) == cudaSuccess &&
-               cudaEventCreateWithFlags(&ctx.ecs, cudaEventDisableTiming) == cudaSuccess &&
-               cudaMalloc(reinterpret_cast<void**>(&ctx.ctl), (kMaxHostChunks + 1) * sizeof(uint32_t)) == cudaSuccess;
-    for (int l = 0; l < kCopyLanes && okc; ++l)
-      okc = cudaStreamCreateWithFlags(&ctx.cin[l], cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&ctx.cout[l], cudaStreamNonBlocking) == cudaSuccess &&
-            cudaEventCreateWithFlags(&ctx.eend[l], cudaEventDisableTiming) == cudaSuccess;
-    for (int i = 0; i < kMaxHostChunks && okc; ++i)
-      okc = cudaEventCreateWithFlags(&ctx.ein[i], cudaEventDisableTiming) == cudaSuccess;
-    if (!okc) return fail(RS_ECUDA, "stream/event/counter creation failed");
-    ctx.dev = dev;
-    // keep stream-ordered allocations cached between calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  }
+  HostCtx* ctxp = nullptr;
+  rc = host_ctx(dev, &ctxp);
+  if (rc != RS_OK) return rc;
+  HostCtx& ctx = *ctxp;
   // wave-column chunks: ~64 per call, at least 16 columns each
   // Fine chunks (kernel-side arrival/release granularity) copied in groups that ramp up
   // and down (1, 1, 2, 4, G, ..., G, 4, 2, 1, 1 fine chunks): a small first group lets
@@ -787,9 +798,14 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
     ck(copy_wave_chunk<T>(dA, A, g, m, lda, rev, v0, v1, cudaMemcpyDeviceToHost, co_), "A copy-out");
   }
   mark(ctx.cout[(ngroups - 1) % lanes], "out_done");
+  // join every copy lane (in and out) into st on every path, success or error: no H2D
+  // copy or arrival write into `mem` / ctx.ctl may still be pending when `mem` returns to
+  // the pool or the next call resets the counters
   for (int l = 0; l < lanes; ++l) {
-    ck(cudaEventRecord(ctx.eend[l], ctx.cout[l]), "event");
-    ck(cudaStreamWaitEvent(st, ctx.eend[l], 0), "wait");
+    cudaEventRecord(ctx.ejoin[l], ctx.cin[l]);
+    cudaStreamWaitEvent(st, ctx.ejoin[l], 0);
+    cudaEventRecord(ctx.eend[l], ctx.cout[l]);
+    cudaStreamWaitEvent(st, ctx.eend[l], 0);
   }
   cudaFreeAsync(mem, st);
   cudaError_t es = cudaStreamSynchronize(st);
@@ -950,6 +966,46 @@ rs_status rs_apply_packed_f32(float* A, int64_t m, int64_t n, int64_t lda, int64
                               int strict, void* workspace, size_t workspace_bytes, void* stream) {
   g_err.clear();
   return apply_packed_impl<float>(A, m, n, lda, k, side, order, kind, strict, workspace, workspace_bytes, stream);
+}
+
+rs_status rs_packed_form(const void* workspace, size_t workspace_bytes, int64_t m, int64_t n, int64_t k,
+                         int side, int kind, int dtype, int64_t* scaled_units, int64_t* total_units, void* stream) {
+  g_err.clear();
+  if (!scaled_units || !total_units) return fail(RS_EINVAL, "null pointer");
+  if (dtype != RS_DTYPE_F64 && dtype != RS_DTYPE_F32) return fail(RS_EINVAL, "dtype must be 0 (f64) or 1 (f32)");
+  Geometry g;
+  rs_status rc = validate(m, n, m > 1 ? m : 1, 0, k, side, RS_ORDER_FORWARD, kind, dtype, false, &g);
+  if (rc != RS_OK) return rc;
+  rc = check_workspace(g, const_cast<void*>(workspace), workspace_bytes);
+  if (rc != RS_OK) return rc;
+  LaunchPlan lp;
+  rc = plan_launch(g, dtype == RS_DTYPE_F64 ? 8 : 4, &lp);
+  if (rc != RS_OK) return rc;
+  const int nw = 2 * (lp.ua + 1);
+  uint32_t flags[2 * (kK + 1) + 2];
+  uint32_t* host = nw <= (int)(sizeof(flags) / sizeof(flags[0])) ? flags : (uint32_t*)malloc(nw * sizeof(uint32_t));
+  if (!host) return fail(RS_ENOMEM, "host buffer");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned char* base = reinterpret_cast<const unsigned char*>(workspace) + g.coef_bytes + g.flags_only;
+  cudaError_t e = cudaMemcpyAsync(host, base, nw * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    if (host != flags) free(host);
+    return fail(RS_ECUDA, std::string("rs_packed_form: ") + cudaGetErrorString(e));
+  }
+  // part 1: the first t1 tiles, ua+1 units each; part 0: the others, ua units each
+  long long scaled = 0;
+  const bool off = scaled_disabled();
+  for (int part = 0; part < 2; ++part) {
+    const long long tiles = part ? lp.t1 : g.tiles - lp.t1;
+    const int ut = lp.ua + part;
+    for (int i = 0; i < ut && tiles > 0; ++i)
+      if (!off && host[part * (lp.ua + 1) + i] == 0u) scaled += tiles;
+  }
+  if (host != flags) free(host);
+  *scaled_units = scaled;
+  *total_units = lp.units;
+  return RS_OK;
 }
 
 rs_status rs_apply_host_f64(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S,

@@ -392,7 +392,8 @@ struct PipeParams {
   long long t1;      // the first t1 tiles hold ua+1 units, the others ua
   const void* coef;  // packed coefficient blocks (see rs_pack_kernel)
   const void* coef_scaled;  // scaled-form blocks (rs_pack_scaled_kernel)
-  const uint32_t* unsafe;   // set by rs_pack_scaled_kernel: scaled form out of safe range
+  const uint32_t* unsafe;   // [2][ua+1] per (sweep partition, unit index): set by rs_pack_scaled_kernel
+                            // when the unit's coefficients are outside the scaled form's safe range
   uint32_t* flags;   // [tiles*k + 1] progress flags of in-place hand-offs, index tile*k + p0
   void* trash;       // 32*R elements: write/read target of lanes past the last row
   int ua;            // units per tile (base)
@@ -612,9 +613,8 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
 // ------------------------------------------------------------------------------------
 // the persistent pipeline kernel
 // ------------------------------------------------------------------------------------
-template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED, bool HS, bool LEFT>
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED_ANY, bool HS, bool LEFT>
 __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned char* smem_raw) {
-  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
@@ -676,6 +676,13 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
       if (slot < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
     }
     const bool self = src != SRC_RING;
+    // arithmetic form of this unit: the scaled (fast Givens) records unless the pack
+    // flagged this unit's coefficients as outside the scaled form's safe range
+    const int part = tile < P.t1 ? 1 : 0;
+    const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
+    auto unit_body = [&](auto scaled_c) {
+    constexpr bool SCALED = decltype(scaled_c)::value;
+    using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
 
     T* grow[R];        // element (row r, column 0) of this lane's lines
     long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
@@ -696,11 +703,9 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     const bool lfull = tile * TR + TR <= P.owners;
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
     // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
-    const int part = tile < P.t1 ? 1 : 0;
     const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
     const CoefT* ubase;
     if constexpr (SCALED) {
-      const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
       ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
               (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
     } else {
@@ -982,16 +987,24 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     }
     for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
     trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
+    };
+    if constexpr (SCALED_ANY) {
+      if (__ldg(P.unsafe + part * (P.ua + 1) + iu) == 0u)
+        unit_body(std::true_type{});
+      else
+        unit_body(std::false_type{});
+    } else {
+      unit_body(std::false_type{});
+    }
   }
 }
 
 // Right side: the original per-block protocol (generic-pointer output, lane-0 branches);
 // it schedules the unrolled body better than the lean protocol under the 128-register
 // budget of 16-warp CTAs.
-template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED, bool HS, bool LEFT>
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED_ANY, bool HS, bool LEFT>
 __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsigned char* smem_raw) {
   static_assert(!LEFT, "right-side protocol");
-  using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
   constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
@@ -1051,6 +1064,13 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
       if (slot < NW - 1 && g + 1 < cr.g1 && unit_to_pos(cr, g + 1) == pos + 1) dst = DST_RING;
     }
     const bool self = src != SRC_RING;
+    // arithmetic form of this unit: the scaled (fast Givens) records unless the pack
+    // flagged this unit's coefficients as outside the scaled form's safe range
+    const int part = tile < P.t1 ? 1 : 0;
+    const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
+    auto unit_body = [&](auto scaled_c) {
+    constexpr bool SCALED = decltype(scaled_c)::value;
+    using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
 
     T* grow[R];        // element (row r, column 0) of this lane's lines
     long long gcs[R];  // column stride; 0 for rows past the matrix (they use the trash slot)
@@ -1071,11 +1091,9 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     const bool lfull = tile * TR + TR <= P.owners;
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
     // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
-    const int part = tile < P.t1 ? 1 : 0;
     const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
     const CoefT* ubase;
     if constexpr (SCALED) {
-      const long long iu = g - tile_first_unit(tile, P.t1, P.ua);
       ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
               (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
     } else {
@@ -1355,6 +1373,15 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     }
     for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
     trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
+    };
+    if constexpr (SCALED_ANY) {
+      if (__ldg(P.unsafe + part * (P.ua + 1) + iu) == 0u)
+        unit_body(std::true_type{});
+      else
+        unit_body(std::false_type{});
+    } else {
+      unit_body(std::false_type{});
+    }
   }
 }
 
@@ -1383,9 +1410,10 @@ __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pip
     mbar_init(bw + FB + 2, 1);
   }
   __syncthreads();
-  // fast mode: the scaled form, unless the pack found coefficients outside its safe range
+  // fast mode: every unit runs the scaled form unless the pack flagged its coefficients
+  // (per unit, P.unsafe) as outside the scaled form's safe range; strict: standard records
   if constexpr (!STRICT) {
-    if (P.use_scaled && *P.unsafe == 0u) {
+    if (P.use_scaled) {
       if constexpr (LEFT || RS_RIGHT_LEAN) {
         pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
       } else {
@@ -1416,9 +1444,6 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
                                                       int nblk, int ua, int nparts, int rev,
                                                       const uint32_t* __restrict__ only_if_unsafe) {
   constexpr int K = kK;
-  // fast mode packs the scaled records first; the standard records are only the fallback
-  // for coefficients outside the scaled form's safe range
-  if (only_if_unsafe != nullptr && *only_if_unsafe == 0u) return;
   const int per_p = nblk * (K + 1);
   for (int row = blockIdx.y; row < nparts * k; row += gridDim.y) {
     const int part = row / k;
@@ -1428,6 +1453,9 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
     int i = (int)(((long long)p * ut) / k);
     while (i + 1 < ut && sweep_start(i + 1, ut, k) <= p) ++i;
     while (i > 0 && sweep_start(i, ut, k) > p) --i;
+    // fast mode packs the scaled records first; the standard records are only the
+    // fallback of the units whose coefficients are outside the scaled form's safe range
+    if (only_if_unsafe != nullptr && only_if_unsafe[part * (ua + 1) + i] == 0u) continue;
     const int p0 = sweep_start(i, ut, k);
     const int kb = sweep_start(i + 1, ut, k) - p0;
     const int l = p - p0;
@@ -1477,7 +1505,8 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
 // (rotation (j-1, p) before (j, p) before (j+1, p)). The column's final scale is applied
 // when the kernel emits it. Records: (tau1, -tau2) at [b][u*kb + l] as in rs_pack_kernel,
 // then the K+1 emission scales of the block. A coefficient that would push a scale or tau
-// outside [2^-256, 2^256] (or c == 0) sets *unsafe and the kernel uses the standard form.
+// outside [2^-256, 2^256] (or c == 0) flags its unit, unsafe[part*(ua+1) + i]: that unit
+// (in every tile) runs the standard form, the other units keep the scaled one.
 // ------------------------------------------------------------------------------------
 template <typename T, bool REFL>
 __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restrict__ out, const T* __restrict__ C,
@@ -1575,7 +1604,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     // column j is emitted at block j/(K+1) + 1, wave j%(K+1)
     const int be = j / (K + 1) + 1, ue = j - (j / (K + 1)) * (K + 1);
     if (be < nblk) reinterpret_cast<T*>(ubase + (size_t)be * brec + (size_t)nr * (K + 1))[ue] = (T)sa;
-    if (bad) atomicOr(unsafe, 1u);
+    if (bad) atomicOr(unsafe + part * (ua + 1) + i, 1u);
   }
 }
 

@@ -75,14 +75,20 @@ def make_workload_inputs(w: Workload, owner_range=None):
     side) of A, generated identically to the full matrix (the generator stream is
     produced in full and sliced, so shards are bit-identical to the full input).
     """
+    # right-side row shards: the C-order normal stream yields rows in order, so the
+    # first o1 rows of it are exactly rows [0, o1) of the full matrix (no need to
+    # generate the rest); left-side column shards need the full stream
+    rows = w.m
+    if owner_range is not None and w.side is Side.RIGHT:
+        rows = owner_range[1]
     if w.index in (1, 2, 3):
         rng = np.random.Generator(np.random.Philox(0))
-        A = rng.standard_normal((w.m, w.n))
+        A = rng.standard_normal((rows, w.n))
         seq = generate_sequence(w.n, w.k, 1)
         C, S = seq.C, seq.S
     elif w.index == 4:
         rng = np.random.Generator(np.random.Philox(0))
-        A = rng.uniform(-1.0, 1.0, size=(w.m, w.n)).astype(np.float32)
+        A = rng.uniform(-1.0, 1.0, size=(rows, w.n)).astype(np.float32)
         th = np.random.Generator(np.random.Philox(1)).uniform(0.0, 2.0 * np.pi, size=(w.n - 1, w.k))
         C, S = np.cos(th).astype(np.float32), np.sin(th).astype(np.float32)
     elif w.index == 5:

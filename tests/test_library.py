@@ -46,13 +46,15 @@ def test_version_and_workspace_formula():
     ws = lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 0)
     # two sweep partitions x 192 sweeps x 457 blocks x 9 waves of 16 B records
     # (standard form) + the same with 5 scale records per block (scaled form),
-    # + 64 tiles (2 rows per lane) x 192 progress flags + unsafe word + trash slot
+    # + 64 tiles (2 rows per lane) x 192 progress flags + the per-unit range words
+    # ([2][k+1] u32: scaled form safe per sweep partition and unit) + trash slot
     nblk = (4096 + 8) // 9 + 1
     coef = -(-2 * 192 * nblk * 9 * 16 // 256) * 256
     scaled = -(-2 * 192 * nblk * 14 * 16 // 256) * 256
     flags = -(-(64 * 192 + 1) * 4 // 256) * 256
     trash = 32 * 4 * 8  # one slot per lane for the widest tile (fp32: 4 rows per lane)
-    assert ws == coef + scaled + flags + 256 + trash
+    unsafe = -(-2 * (192 + 1) * 4 // 256) * 256
+    assert ws == coef + scaled + flags + unsafe + trash
     assert ws % 256 == 0
     assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 1, 0) > ws  # reflector records are 32 B
     # fp32: the same 16-byte record blocks (paired rotations) and tiles
