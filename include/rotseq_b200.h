@@ -149,6 +149,21 @@ rs_status rs_apply_host_f32(float* A, int64_t m, int64_t n, int64_t lda,
                             const float* C, const float* S, int64_t ldcs, int64_t k,
                             int side, int order, int kind, int strict, void* stream);
 
+/* Micro-kernel API (the reference's kernel_wave_apply, kernels.py:335-371): apply n_waves
+ * waves of k_r transforms to a panel of m_r rows and n_cols columns, column j at
+ * panel + j*ld with its m_r rows contiguous (the reference's C-contiguous (n_cols, m_r)
+ * panel is ld = m_r). Wave w, lane l rotates columns (col0 + w + k_r - 1 - l, +1) with
+ * ct[w*k_r + l], st[w*k_r + l] (wave-major tiles, kernels.py:12-13). Requires
+ * n_cols - col0 >= n_waves + k_r. Strict arithmetic is bit-identical to the reference's
+ * strict build; device pointers, asynchronous on `stream`. kernel_edge_apply
+ * (kernels.py:374-410) is a sequence of k_r = 1 calls. */
+rs_status rs_wave_apply_f64(double* panel, int64_t m_r, int64_t n_cols, int64_t ld, const double* ct,
+                            const double* st, int64_t n_waves, int64_t k_r, int64_t col0, int kind, int strict,
+                            void* stream);
+rs_status rs_wave_apply_f32(float* panel, int64_t m_r, int64_t n_cols, int64_t ld, const float* ct,
+                            const float* st, int64_t n_waves, int64_t k_r, int64_t col0, int kind, int strict,
+                            void* stream);
+
 /* Launch geometry the pipeline would use for this problem on the current device
  * (for benchmarks / roofline accounting). Any out-pointer may be NULL. */
 rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype,

@@ -184,3 +184,41 @@ def upcast_reference(A32, C32, S32, **kw) -> np.ndarray:
     A = np.asfortranarray(A32, dtype=np.float64)
     apply_naive(A, np.asarray(C32, dtype=np.float64), np.asarray(S32, dtype=np.float64), **kw)
     return A
+
+
+def wave_apply(panel, ct, st, n_waves: int, k_r: int, col0: int = 0, kind: str = "rotation") -> None:
+    """Micro-kernel semantics (``_kern_generic_py``, kernels.py:81-103) on a C-contiguous
+    (n_cols, m_r) panel, vectorised over the m_r rows: wave w, lane l rotates columns
+    (col0 + w + k_r - 1 - l, +1) with ct/st[w * k_r + l]. Plain IEEE mul/add in the
+    reference's expression order, so strict results are bit-identical."""
+    P = panel
+    for w in range(n_waves):
+        for lane in range(k_r):
+            c = ct[w * k_r + lane]
+            s = st[w * k_r + lane]
+            j = col0 + w + k_r - 1 - lane
+            xv = P[j].copy()
+            yv = P[j + 1].copy()
+            if kind == "reflector":
+                d = c - s
+                e = c + s
+                wv = s * (xv + yv)
+                P[j] = wv + d * xv
+                P[j + 1] = wv - e * yv
+            else:
+                t = c * xv + s * yv
+                P[j + 1] = c * yv - s * xv
+                P[j] = t
+
+
+def edge_apply(panel, C, S, p0: int, k_chunk: int, triangle: str, kind: str = "rotation") -> None:
+    """Startup / shutdown triangles as k_r = 1 passes (kernel_edge_apply, kernels.py:374-410)."""
+    n = panel.shape[0]
+    if triangle == "startup":
+        for pp in range(k_chunk - 1):
+            run = k_chunk - 1 - pp
+            wave_apply(panel, C[0:run, p0 + pp], S[0:run, p0 + pp], run, 1, 0, kind)
+    else:
+        for pp in range(1, k_chunk):
+            q0 = n - 1 - pp
+            wave_apply(panel, C[q0:n - 1, p0 + pp], S[q0:n - 1, p0 + pp], pp, 1, q0, kind)

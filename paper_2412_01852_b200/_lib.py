@@ -48,6 +48,8 @@ EXPORTS = (
     "rs_packed_form",
     "rs_apply_host_f64",
     "rs_apply_host_f32",
+    "rs_wave_apply_f64",
+    "rs_wave_apply_f32",
     "rs_launch_count",
     "rs_debug_set_trace",
     "rs_fma_peak_tflops",
@@ -90,6 +92,10 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i32, i32, i32, i32, vp]
+    for name in ("rs_wave_apply_f64", "rs_wave_apply_f32"):
+        fn = getattr(lib, name)
+        fn.restype = i32
+        fn.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i64, i32, i32, vp]
     lib.rs_packed_form.restype = i32
     lib.rs_packed_form.argtypes = [vp, sz, i64, i64, i64, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
     lib.rs_plan_info.restype = i32

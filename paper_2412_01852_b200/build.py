@@ -72,7 +72,8 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
         for t, s, r in VARIANTS:
             obj = os.path.join(tmpdir, f"pipe_{t}_{s}_{r}.o")
             jobs.append((obj, [nvcc, *NVCC_FLAGS, *extra, *inc, f"-DRS_VARIANT_T={t}", f"-DRS_VARIANT_STRICT={s}",
-                               f"-DRS_VARIANT_REFL={r}", "-c", "-o", obj, VARIANT_SRC]))
+                               f"-DRS_VARIANT_REFL={r}", f"-DRS_VARIANT_F32={int(t == 'float')}", "-c", "-o", obj,
+                               VARIANT_SRC]))
         with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
             logs = list(pool.map(lambda j: _run(j[1]), jobs))
         fd, tmp = tempfile.mkstemp(suffix=".so", dir=os.path.dirname(out))

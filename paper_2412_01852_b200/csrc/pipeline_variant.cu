@@ -11,9 +11,9 @@
 
 namespace rsk {
 
-template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT>
+template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT, int K>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) {
-  auto kern = rs_pipeline_kernel<T, kK, rows_for(sizeof(T)), STRICT, REFL, HS, LEFT>;
+  auto kern = rs_pipeline_kernel<T, K, rows_for(sizeof(T)), STRICT, REFL, HS, LEFT>;
   static std::atomic<int> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -28,12 +28,17 @@ cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) 
   return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
-#define RS_INST(HS, LEFT)                                                                                 \
-  template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, HS, LEFT>( \
+#define RS_INST(HS, LEFT, K)                                                                                  \
+  template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, HS, LEFT, K>( \
       const cudaLaunchConfig_t&, const PipeParams&);
-RS_INST(false, false)
-RS_INST(true, false)
-RS_INST(false, true)
-RS_INST(true, true)
+RS_INST(false, false, 8)
+RS_INST(true, false, 8)
+RS_INST(false, true, 8)
+RS_INST(true, true, 8)
+// the 16-sweep window (right side, fp32 only: a 17-column window of 2 rows is 34 registers)
+#if RS_VARIANT_F32 && RS_F32_WIDE
+RS_INST(false, false, 16)
+RS_INST(true, false, 16)
+#endif
 
 }  // namespace rsk

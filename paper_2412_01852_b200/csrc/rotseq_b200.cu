@@ -77,6 +77,7 @@ struct Geometry {
   long long pairs = 0;  // (tile, sweep) pairs = tiles * k
   int nchunk = 0;
   int nblk = 0;
+  int kw = kK;  // sweeps per unit window: kK, or kKWide (fp32, right side, wide units)
   size_t coef_rec = 0;
   size_t std_bytes = 0;     // standard records (both sweep partitions)
   size_t coef_bytes = 0;    // standard + scaled records
@@ -84,6 +85,7 @@ struct Geometry {
   size_t unsafe_bytes = 0;  // per-unit "outside the scaled form's range" words, [2][ua+1]
   size_t flag_bytes = 0;    // flags + unsafe words + trash slot
   bool left = false;
+  bool refl = false;
   bool streaming = false;  // host streaming (rs_apply_host_*): input-bound, plain plans only
 };
 
@@ -127,6 +129,7 @@ cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t st) {
 bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int kind, int dtype, Geometry* g) {
   const bool left = side == RS_SIDE_LEFT;
   g->left = left;
+  g->refl = kind == RS_KIND_REFLECTOR;
   g->owners = left ? n : m;
   g->len = (int)(left ? m : n);
   g->os = left ? lda : 1;
@@ -135,14 +138,21 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   const int towners = tile_owners(dtype == RS_DTYPE_F64 ? 8 : 4);
   g->tiles = (g->owners + towners - 1) / towners;
   g->pairs = g->tiles * g->k;
-  g->nchunk = (g->len + kK) / (kK + 1);
+  // the 16-sweep window: fp32, right side, and every unit of the full-width split at
+  // least 9 sweeps wide (the wide kernel is compiled for widths 9..16)
+  g->kw = kK;
+  if (RS_F32_WIDE && dtype == RS_DTYPE_F32 && !left && k >= kKWide && !getenv("RS_F32_K8")) {
+    const int64_t ut0 = (k + kKWide - 1) / kKWide;
+    if (k / ut0 >= kb_min(kKWide)) g->kw = kKWide;
+  }
+  g->nchunk = (g->len + g->kw) / (g->kw + 1);
   g->nblk = g->nchunk + 1;
   const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
   g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 * tsz : 16);
   // two sweep partitions (ua and ua+1 units per tile) of k * nblk * (K+1) records each
-  g->std_bytes = align_up(2 * (size_t)g->k * g->nblk * (kK + 1) * g->coef_rec, 256);
+  g->std_bytes = align_up(2 * (size_t)g->k * g->nblk * (g->kw + 1) * g->coef_rec, 256);
   // scaled form: per partition k*nblk*(K+1) records + <= k*nblk*kScaleRecs scale records
-  g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (kK + 1 + kScaleRecs) * 16, 256);
+  g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (g->kw + 1 + kScaleRecs) * 16, 256);
   g->flags_only = align_up((size_t)(g->pairs + 1) * sizeof(uint32_t), 256);
   g->unsafe_bytes = align_up(2 * (size_t)(g->k + 1) * sizeof(uint32_t), 256);  // ua + 1 <= k + 1
   g->flag_bytes = g->flags_only + g->unsafe_bytes + kTrashBytes;
@@ -159,11 +169,11 @@ struct LaunchPlan {
   int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units; 3: aligned
 };
 
-size_t smem_per_warp(size_t tsz, size_t coef_rec, bool left) {
-  size_t cbuf = (size_t)(kK + 1) * kK * coef_rec;  // == coef_buf_bytes<T, REFL>()
-  const size_t scl = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
-  if (scl > cbuf) cbuf = scl;
-  return 2 * coef_blocks_per_buf(left) * cbuf + (size_t)stages_for(tsz) * (kK + 1) * tile_owners(tsz) * tsz + ctl_words(stages_for(tsz), left) * sizeof(uint64_t);
+size_t smem_per_warp(size_t tsz, size_t coef_rec, bool left, int K, bool refl) {
+  // == coef_buf_bytes<T, REFL, K>() (fp32 rotation records hold two lanes each)
+  const size_t cbuf = coef_block_bytes(K, tsz == 4 && !refl, coef_rec);
+  return 2 * coef_blocks_per_buf(left) * cbuf + (size_t)stages_for(tsz) * (K + 1) * tile_owners(tsz) * tsz +
+         ctl_words(stages_for(tsz), left) * sizeof(uint64_t);
 }
 
 // Grid of G <= #SMs persistent CTAs and U = 4*G*q units (q per SM sub-partition, each
@@ -176,7 +186,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return fail(RS_ECUDA, "cudaDeviceGetAttribute failed");
-  const size_t per = smem_per_warp(tsz, g.coef_rec, g.left);
+  const size_t per = smem_per_warp(tsz, g.coef_rec, g.left, g.kw, g.refl);
   // one extra control block: the (never dereferenced) out-ring words of the last warp
   const size_t ctl = ctl_words(stages_for(tsz), g.left) * sizeof(uint64_t);
   int cap = (int)((optin - ctl) / per);
@@ -207,11 +217,17 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   if (!hooks && !g.streaming && !getenv("RS_NO_ALIGNED_PLAN")) {
     long long bestG = 0, bestU = 0;
     int bestNW = 0;
-    const int ut0 = (g.k + kK - 1) / kK;
+    const int ut0 = (g.k + g.kw - 1) / g.kw;
+    // developer knobs (measurements): force the chain length / warps per CTA
+    const int force_ut = getenv("RS_ALIGNED_UT") ? atoi(getenv("RS_ALIGNED_UT")) : 0;
+    const int force_nw = getenv("RS_ALIGNED_NW") ? atoi(getenv("RS_ALIGNED_NW")) : 0;
     for (int ut = ut0; ut <= 2 * ut0 && ut <= g.k; ++ut) {
       if (g.k % ut != 0) continue;
+      if (g.k / ut < kb_min(g.kw)) continue;  // wide window: units of >= 9 sweeps only
+      if (force_ut > 0 && ut != force_ut) continue;
       const long long U = g.tiles * ut;
       for (int nw = cap; nw >= 8; nw -= 4) {
+        if (force_nw > 0 && nw != force_nw) continue;
         if (!(ut % nw == 0 || nw % ut == 0) || U % nw != 0) continue;
         const long long cr = U / nw;  // CTA-rounds
         long long r = (cr + grid - 1) / grid;
@@ -233,7 +249,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
       return RS_OK;
     }
   }
-  const long long umin = g.tiles * ((g.k + kK - 1) / kK);
+  const long long umin = g.tiles * ((g.k + g.kw - 1) / g.kw);
   const long long gneed = (umin + 3) / 4;
   if (gneed < grid) grid = gneed;
   if (grid < 1) grid = 1;
@@ -254,6 +270,9 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     const int v = atoi(ev);
     if (v == 1 || v == 2) mode = v;
   }
+  // the wide window runs units of >= 9 sweeps only: full-width units (mode 2) unless
+  // the few-units split keeps every unit that wide
+  if (g.kw > kK && (double)g.k * g.tiles / (double)(4 * grid * q) < kb_min(g.kw) + 1) mode = 2;
   long long U = mode == 1 ? 4 * grid * q : umin;
   if (U > g.pairs) U = g.pairs;  // at least one sweep per unit
   // the fewest rounds of <= cap warps, spread evenly (equal rounds keep every round's
@@ -289,7 +308,7 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
   rs_status rc = plan_launch(g, sizeof(T), &lp);
   if (rc != RS_OK) return rc;
   const int nparts = lp.t1 > 0 ? 2 : 1;
-  const int per_p = g.nblk * (kK + 1);
+  const int per_p = g.nblk * (g.kw + 1);
   int bx = (per_p + 255) / 256;
   if (bx > 64) bx = 64;
   const int rows = nparts * g.k;
@@ -309,12 +328,23 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
     if (e0 != cudaSuccess) return fail(RS_ECUDA, std::string("cudaMemsetAsync: ") + cudaGetErrorString(e0));
     const int srows = nparts * (lp.ua + 1);
     const int sy = srows < 65535 ? srows : 65535;
-    rs_pack_scaled_kernel<T, REFL><<<dim3((unsigned)((g.len + 127) / 128), (unsigned)sy), 128, 0, st>>>(
-        reinterpret_cast<SCoef<T>*>(base + g.std_bytes), C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts, rev, unsafe);
+    const dim3 sgrid((unsigned)((g.len + 127) / 128), (unsigned)sy);
+    SCoef<T>* const sout = reinterpret_cast<SCoef<T>*>(base + g.std_bytes);
+    if (g.kw == kKWide)
+      rs_pack_scaled_kernel<T, REFL, kKWide><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua,
+                                                                    nparts, rev, unsafe);
+    else
+      rs_pack_scaled_kernel<T, REFL, kK><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts,
+                                                                rev, unsafe);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  rs_pack_kernel<T, REFL><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(
-      coef, C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts, rev, scaled && std_only_if_unsafe ? unsafe : nullptr);
+  const uint32_t* const only = scaled && std_only_if_unsafe ? unsafe : nullptr;
+  if (g.kw == kKWide)
+    rs_pack_kernel<T, REFL, kKWide><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
+                                                                                      g.nblk, lp.ua, nparts, rev, only);
+  else
+    rs_pack_kernel<T, REFL, kK><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
+                                                                                  g.nblk, lp.ua, nparts, rev, only);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
@@ -384,11 +414,20 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool left = g.os != 1;  // owners are columns: owner-major rings, coalesced A I/O
-  if (hs)
-    e = left ? launch_pipeline<T, STRICT, REFL, true, true>(cfg, P) : launch_pipeline<T, STRICT, REFL, true, false>(cfg, P);
-  else
-    e = left ? launch_pipeline<T, STRICT, REFL, false, true>(cfg, P)
-             : launch_pipeline<T, STRICT, REFL, false, false>(cfg, P);
+  if (g.kw == kKWide) {
+    if constexpr (sizeof(T) == 4 && RS_F32_WIDE) {
+      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, kKWide>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false, kKWide>(cfg, P);
+    } else {
+      return fail(RS_EUNSUPPORTED, "16-sweep window is built for fp32 right-side launches only");
+    }
+  } else if (hs) {
+    e = left ? launch_pipeline<T, STRICT, REFL, true, true, kK>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, true, false, kK>(cfg, P);
+  } else {
+    e = left ? launch_pipeline<T, STRICT, REFL, false, true, kK>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false, kK>(cfg, P);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pipeline launch: ") + cudaGetErrorString(e));
   return RS_OK;
@@ -824,6 +863,62 @@ rs_status apply_host_impl(T* A, int64_t m, int64_t n, int64_t lda, const T* C, c
   return RS_OK;
 }
 
+// micro-kernel API launcher (kernel_wave_apply, kernels.py:335-371)
+template <typename T, bool STRICT, bool REFL, int KR>
+cudaError_t launch_wave_kr(T* P, long long m_r, long long ld, const T* ct, const T* st, long long n_waves,
+                           long long col0, cudaStream_t s) {
+  const size_t smem = (size_t)2 * kWaveChunkBlocks * (KR + 1) * KR * sizeof(T);
+  const unsigned blocks = (unsigned)((m_r + 127) / 128);
+  rs_wave_kernel<T, KR, STRICT, REFL><<<blocks, 128, smem, s>>>(P, m_r, ld, ct, st, n_waves, col0);
+  return cudaGetLastError();
+}
+template <typename T, bool STRICT, bool REFL>
+cudaError_t launch_wave(T* P, long long m_r, long long ld, const T* ct, const T* st, long long n_waves, int k_r,
+                        long long col0, cudaStream_t s) {
+  switch (k_r) {
+    case 1: return launch_wave_kr<T, STRICT, REFL, 1>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 2: return launch_wave_kr<T, STRICT, REFL, 2>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 3: return launch_wave_kr<T, STRICT, REFL, 3>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 4: return launch_wave_kr<T, STRICT, REFL, 4>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 5: return launch_wave_kr<T, STRICT, REFL, 5>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 6: return launch_wave_kr<T, STRICT, REFL, 6>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 7: return launch_wave_kr<T, STRICT, REFL, 7>(P, m_r, ld, ct, st, n_waves, col0, s);
+    case 8: return launch_wave_kr<T, STRICT, REFL, 8>(P, m_r, ld, ct, st, n_waves, col0, s);
+    default: {
+      const unsigned blocks = (unsigned)((m_r + 127) / 128);
+      rs_wave_kernel_wide<T, STRICT, REFL><<<blocks, 128, 0, s>>>(P, m_r, ld, ct, st, n_waves, k_r, col0);
+      return cudaGetLastError();
+    }
+  }
+}
+template <typename T>
+rs_status wave_impl(T* P, int64_t m_r, int64_t n_cols, int64_t ld, const T* ct, const T* st, int64_t n_waves,
+                    int64_t k_r, int64_t col0, int kind, int strict, void* stream) {
+  if (kind != RS_KIND_ROTATION && kind != RS_KIND_REFLECTOR)
+    return fail(RS_EINVAL, "kind must be 0 (rotation) or 1 (reflector)");
+  if (m_r < 0 || n_cols < 0 || n_waves < 0 || col0 < 0) return fail(RS_EINVAL, "sizes must be non-negative");
+  if (k_r < 1) return fail(RS_EINVAL, "kernel shape must be positive (k_r >= 1)");
+  if (k_r > (1 << 20)) return fail(RS_EUNSUPPORTED, "k_r larger than 2^20");
+  if (ld < (m_r > 1 ? m_r : 1)) return fail(RS_EINVAL, "ld must be >= max(1, m_r)");
+  if (n_cols - col0 < n_waves + k_r)
+    return fail(RS_EINVAL, "panel has " + std::to_string(n_cols - col0) + " usable columns, need " +
+                               std::to_string(n_waves + k_r) + " for " + std::to_string(n_waves) + " waves of " +
+                               std::to_string(k_r));
+  if (m_r == 0 || n_waves == 0) return RS_OK;
+  if (!P || !ct || !st) return fail(RS_EINVAL, "null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (strict)
+    e = kind == RS_KIND_REFLECTOR ? launch_wave<T, true, true>(P, m_r, ld, ct, st, n_waves, (int)k_r, col0, s)
+                                  : launch_wave<T, true, false>(P, m_r, ld, ct, st, n_waves, (int)k_r, col0, s);
+  else
+    e = kind == RS_KIND_REFLECTOR ? launch_wave<T, false, true>(P, m_r, ld, ct, st, n_waves, (int)k_r, col0, s)
+                                  : launch_wave<T, false, false>(P, m_r, ld, ct, st, n_waves, (int)k_r, col0, s);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("wave kernel launch: ") + cudaGetErrorString(e));
+  return RS_OK;
+}
+
 template <typename T>
 rs_status fma_peak(double* tflops, cudaStream_t st) {
   int dev = 0, sms = 0;
@@ -929,7 +1024,7 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
   if (grid_ctas) *grid_ctas = lp.grid;
   if (warps_per_cta) *warps_per_cta = lp.nw;
   if (units) *units = lp.units;
-  if (band_width) *band_width = kK;
+  if (band_width) *band_width = g.kw;
   if (rows_per_tile) *rows_per_tile = tile_owners(dtype == RS_DTYPE_F64 ? 8 : 4);
   if (smem_bytes) *smem_bytes = lp.smem;
   return RS_OK;
@@ -1017,6 +1112,19 @@ rs_status rs_apply_host_f32(float* A, int64_t m, int64_t n, int64_t lda, const f
                             int64_t ldcs, int64_t k, int side, int order, int kind, int strict, void* stream) {
   g_err.clear();
   return apply_host_impl<float>(A, m, n, lda, C, S, ldcs, k, side, order, kind, strict, stream);
+}
+
+rs_status rs_wave_apply_f64(double* panel, int64_t m_r, int64_t n_cols, int64_t ld, const double* ct,
+                            const double* st, int64_t n_waves, int64_t k_r, int64_t col0, int kind, int strict,
+                            void* stream) {
+  g_err.clear();
+  return wave_impl<double>(panel, m_r, n_cols, ld, ct, st, n_waves, k_r, col0, kind, strict, stream);
+}
+rs_status rs_wave_apply_f32(float* panel, int64_t m_r, int64_t n_cols, int64_t ld, const float* ct,
+                            const float* st, int64_t n_waves, int64_t k_r, int64_t col0, int kind, int strict,
+                            void* stream) {
+  g_err.clear();
+  return wave_impl<float>(panel, m_r, n_cols, ld, ct, st, n_waves, k_r, col0, kind, strict, stream);
 }
 
 rs_status rs_debug_set_trace(void* device_ptr) {

@@ -21,7 +21,13 @@ namespace rsk {
 // ------------------------------------------------------------------------------------
 // compile-time geometry
 // ------------------------------------------------------------------------------------
-constexpr int kK = 8;          // max sweeps per unit (lanes of the wavefront)
+constexpr int kK = 8;          // sweeps per unit window (lanes of the wavefront), default
+// fp32 right-side launches whose units all span >= 9 sweeps use a 16-sweep window
+// (RS_F32_WIDE=0 compiles it out; the env RS_F32_K8=1 disables it at run time)
+#ifndef RS_F32_WIDE
+#define RS_F32_WIDE 1
+#endif
+constexpr int kKWide = 16;
 // owners (rows) per thread, per element size. 2 for both: fp32 with 4 rows per thread (8
 // warps of 255 registers per CTA) measured 30.3 TF/s at config 4 against 31.1 with 2.
 #ifndef RS_ROWS_F32
@@ -59,6 +65,12 @@ __host__ __device__ constexpr int full_bars(int stages, bool left) { return left
 __host__ __device__ constexpr int ctl_words(int stages, bool left) { return full_bars(stages, left) + 3; }
 #ifndef RS_RIGHT_LEAN
 #define RS_RIGHT_LEAN 0
+#endif
+#ifndef RS_STS_DIRECT
+#define RS_STS_DIRECT 1
+#endif
+#ifndef RS_FMA_PAIRED
+#define RS_FMA_PAIRED 0
 #endif
 #ifndef RS_MAX_WARPS
 #define RS_MAX_WARPS 16
@@ -131,11 +143,17 @@ __device__ __forceinline__ CoefT lane_coef(const CoefT* __restrict__ wrec, int l
 }
 
 // bytes of one per-warp coefficient buffer (two per warp: double buffering)
-template <typename T, bool REFL>
-__host__ __device__ constexpr size_t coef_buf_bytes() {
-  const size_t std_bytes = (size_t)(kK + 1) * kK * sizeof(Coef<T, REFL>);
-  const size_t scl_bytes = ((size_t)(kK + 1) * kK + kScaleRecs) * 16;
+// (one block of a unit of the widest width K: (K+1) waves of recs_per_wave(K) records, plus
+// the scaled form's column scales; host mirror: smem_per_warp in rotseq_b200.cu)
+__host__ __device__ constexpr size_t coef_block_bytes(int K, bool pair, size_t rec) {
+  const size_t std_bytes = (size_t)(K + 1) * (pair ? (K + 1) / 2 : K) * rec;
+  const size_t scl_bytes = ((size_t)(K + 1) * (pair ? (K + 1) / 2 : K) + kScaleRecs) * 16;
   return std_bytes > scl_bytes ? std_bytes : scl_bytes;
+}
+template <typename T, bool REFL, int K = kK>
+__host__ __device__ constexpr size_t coef_buf_bytes() {
+  static_assert((K + 1) * sizeof(T) <= kScaleRecs * 16, "a block's column scales must fit kScaleRecs records");
+  return coef_block_bytes(K, kPairRecs<T, REFL>, sizeof(Coef<T, REFL>));
 }
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -483,6 +501,21 @@ __host__ __device__ __forceinline__ long long unit_to_pos(const CtaRange& r, lon
   return g >= r.g1 - r.nl ? g - (r.g1 - r.nl) : g - r.g0 + r.nl;
 }
 
+// Unit widths a window of K sweeps is compiled for: every width 1..8 for the 8-sweep
+// window; the 16-sweep window (fp32, right side) only runs units of 9..16 sweeps (the
+// planner guarantees it; narrower units use the 8-sweep window).
+__host__ __device__ constexpr int kb_min(int K) { return K > 8 ? 9 : 1; }
+template <int K, int KMIN, int KB = K, typename F>
+__device__ __forceinline__ void dispatch_width(int Kb, F&& f) {
+  if constexpr (KB >= KMIN) {
+    if (Kb == KB || KB == KMIN) {
+      f(std::integral_constant<int, KB>{});
+    } else {
+      dispatch_width<K, KMIN, KB - 1>(Kb, f);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // one block of K+1 waves for one warp (fully unrolled; window slots are compile-time)
 //   block b covers waves t = b(K+1)-1 .. b(K+1)+K-1. At the start of wave u it emits
@@ -598,12 +631,24 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
         cf = cq[t % CD];
         if (t + CD < NSTEP) cq[t % CD] = lane_coef<PAIR>(cb + ((t + CD) / NL) * NR, (t + CD) % NL);
       }
+      if constexpr (SCALED && RS_FMA_PAIRED) {
+        // the R rows' FMAs with the same multiplier back to back (tau1 for every row, then
+        // tau2): the shared coefficient register can come from the operand reuse cache
+        T xo[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if constexpr (SCALED) {
-          xform_scaled<T>(w[r][sx], w[r][sy], cf);
-        } else {
-          xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+        for (int r = 0; r < R; ++r) xo[r] = w[r][sx];
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[r][sx] = fma_rn(cf.c, w[r][sy], xo[r]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) w[r][sy] = fma_rn(cf.s, xo[r], w[r][sy]);
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if constexpr (SCALED) {
+            xform_scaled<T>(w[r][sx], w[r][sy], cf);
+          } else {
+            xform<T, STRICT, REFL>(w[r][sx], w[r][sy], cf);
+          }
         }
       }
     }
@@ -617,7 +662,7 @@ template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED_ANY, boo
 __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned char* smem_raw) {
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
-  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL, K>();  // one coefficient buffer (bytes)
   constexpr int S = stages_for(sizeof(T));
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
@@ -695,7 +740,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     }
     // LEFT coalesced chunk copies: this lane's first element e = lane is owner lo0, column
     // lv0; each step of 32 elements advances 3 owners + 5 columns (wrapping past K+1)
-    static_assert(32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
+    static_assert(!LEFT || 32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
     const int lo0 = lane / (K + 1), lv0 = lane - lo0 * (K + 1);
     const long long lstep = 3 * P.os + (32 - 3 * (K + 1)) * P.cs;
     const long long lwrap = P.os - (K + 1) * P.cs;
@@ -975,16 +1020,10 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
     const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
     block(0, I8{}, T_{});
-    switch (Kb) {
-      case 8: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 8>{}, F_{}); break;
-      case 7: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 7>{}, F_{}); break;
-      case 6: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 6>{}, F_{}); break;
-      case 5: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 5>{}, F_{}); break;
-      case 4: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 4>{}, F_{}); break;
-      case 3: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 3>{}, F_{}); break;
-      case 2: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 2>{}, F_{}); break;
-      default: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 1>{}, F_{}); break;
-    }
+    // interior blocks with the unit width as a compile-time constant (one loop body per width)
+    dispatch_width<K, kb_min(K)>(Kb, [&](auto kb_c) {
+      for (int b = 1; b < interior_end; ++b) block(b, kb_c, F_{});
+    });
     for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
     trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
     };
@@ -1007,7 +1046,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   static_assert(!LEFT, "right-side protocol");
   constexpr int TR = 32 * R;
   constexpr int CHUNK = (K + 1) * TR;  // ring chunk: K+1 columns x TR owners
-  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();  // one coefficient buffer (bytes)
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL, K>();  // one coefficient buffer (bytes)
   constexpr int S = stages_for(sizeof(T));
   constexpr int FA = S - 1;  // self-fill distance in chunks
   static_assert(FA == 1 || FA == 2, "ring depth must be 2 or 3 chunks");
@@ -1083,7 +1122,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     }
     // LEFT coalesced chunk copies: this lane's first element e = lane is owner lo0, column
     // lv0; each step of 32 elements advances 3 owners + 5 columns (wrapping past K+1)
-    static_assert(32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
+    static_assert(!LEFT || 32 == 3 * (K + 1) + 5, "coalesced owner-major copy assumes K + 1 = 9");
     const int lo0 = lane / (K + 1), lv0 = lane - lo0 * (K + 1);
     const long long lstep = 3 * P.os + (32 - 3 * (K + 1)) * P.cs;
     const long long lwrap = P.os - (K + 1) * P.cs;
@@ -1273,7 +1312,14 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
         uint64_t* const sub_out = (SUB > 1 && outring && has_out) ? &full_out[(oseq % S) * SUB] : nullptr;
         const uint32_t sub_par = (iseq / S) & 1u;
         if (outring && P.ring_sts) {
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, op[0], b, len, Kb,
+#if RS_STS_DIRECT
+          // the consumer's ring slot addressed from the shared window itself (not through
+          // op[], which also holds global pointers): plain STS with shared-space alias info
+          T* const obase_s = rout + (oseq % S) * CHUNK + lane;
+#else
+          T* const obase_s = op[0];
+#endif
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, obase_s, b, len, Kb,
                                                                           lane, b < nchunk, b >= 1, sub_in, sub_par,
                                                                           sub_out);
         } else {
@@ -1361,16 +1407,10 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
     const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
     block(0, I8{}, T_{});
-    switch (Kb) {
-      case 8: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 8>{}, F_{}); break;
-      case 7: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 7>{}, F_{}); break;
-      case 6: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 6>{}, F_{}); break;
-      case 5: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 5>{}, F_{}); break;
-      case 4: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 4>{}, F_{}); break;
-      case 3: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 3>{}, F_{}); break;
-      case 2: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 2>{}, F_{}); break;
-      default: for (int b = 1; b < interior_end; ++b) block(b, std::integral_constant<int, 1>{}, F_{}); break;
-    }
+    // interior blocks with the unit width as a compile-time constant (one loop body per width)
+    dispatch_width<K, kb_min(K)>(Kb, [&](auto kb_c) {
+      for (int b = 1; b < interior_end; ++b) block(b, kb_c, F_{});
+    });
     for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
     trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
     };
@@ -1392,7 +1432,7 @@ template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
 __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
   constexpr int S = stages_for(sizeof(T));
   constexpr int NBAR = ctl_words(S, LEFT);
-  constexpr size_t CBUF = coef_buf_bytes<T, REFL>();
+  constexpr size_t CBUF = coef_buf_bytes<T, REFL, K>();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * coef_blocks_per_buf(LEFT) * CBUF +
@@ -1438,12 +1478,11 @@ __global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pip
 // (blocking.py:364-373). One bulk copy stages a block. Reverse order mirrors j and
 // negates S (rotation) or C (reflector): both exact in IEEE arithmetic.
 // ------------------------------------------------------------------------------------
-template <typename T, bool REFL>
+template <typename T, bool REFL, int K>
 __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
                                                       const T* __restrict__ Sm, long long ldcs, int len, int k,
                                                       int nblk, int ua, int nparts, int rev,
                                                       const uint32_t* __restrict__ only_if_unsafe) {
-  constexpr int K = kK;
   const int per_p = nblk * (K + 1);
   for (int row = blockIdx.y; row < nparts * k; row += gridDim.y) {
     const int part = row / k;
@@ -1508,12 +1547,11 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
 // outside [2^-256, 2^256] (or c == 0) flags its unit, unsafe[part*(ua+1) + i]: that unit
 // (in every tile) runs the standard form, the other units keep the scaled one.
 // ------------------------------------------------------------------------------------
-template <typename T, bool REFL>
+template <typename T, bool REFL, int K>
 __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restrict__ out, const T* __restrict__ C,
                                                              const T* __restrict__ Sm, long long ldcs, int len, int k,
                                                              int nblk, int ua, int nparts, int rev,
                                                              uint32_t* __restrict__ unsafe) {
-  constexpr int K = kK;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= len) return;
   // scales and taus are formed in fp64 (for fp32 too) and rounded once when stored
@@ -1546,9 +1584,9 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
                       (size_t)i * nblk * kScaleRecs;
     // the unit's coefficients of rotations (j-1, p), (j, p), (j+1, p), loaded up front
     // (independent loads in flight together; only c is needed for the neighbours)
-    double cl[kK], cj[kK], sj[kK], cr[kK];
+    double cl[K], cj[K], sj[K], cr[K];
 #pragma unroll
-    for (int l = 0; l < kK; ++l) {
+    for (int l = 0; l < K; ++l) {
       cl[l] = cj[l] = cr[l] = 1.0;
       sj[l] = 0.0;
       if (l < kb) {
@@ -1560,11 +1598,11 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     }
     // running scales of columns j and j+1 (a short multiply chain), then the taus of all
     // kb rotations independently (their divisions overlap)
-    double sal[kK], sbl[kK];
+    double sal[K], sbl[K];
     double sa = 1, sb = 1;
     bool bad = false;
 #pragma unroll
-    for (int l = 0; l < kK; ++l) {
+    for (int l = 0; l < K; ++l) {
       if (l < kb) {
         if (j >= 1) sa *= REFL ? -cl[l] : cl[l];  // rotation (j-1, p) touched column j as its y
         sal[l] = sa;
@@ -1578,7 +1616,7 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
       }
     }
 #pragma unroll
-    for (int l = 0; l < kK; ++l) {
+    for (int l = 0; l < K; ++l) {
       if (l < kb && j <= len - 2) {
         const double c = cj[l], s = sj[l];
         // tau1 = s*sb / (c*sa), tau2 = s*sa / (c*sb), with one division
@@ -1639,6 +1677,99 @@ __global__ void rs_naive_kernel(T* __restrict__ A, long long os, long long cs, l
 }
 
 // ------------------------------------------------------------------------------------
+// micro-kernel API (the reference's kernel_wave_apply, kernels.py:81-103, 335-371): a
+// panel of m_r rows, column j at P + j*ld (rows contiguous); wave w, lane l rotates
+// columns (col0 + w + KR-1-l, +1) with ct/st[w*KR + l] (wave-major tiles). One thread per
+// row. The coefficient tiles are staged through shared memory in chunks of
+// kWaveChunkBlocks*(KR+1) waves; each thread keeps the (KR+1)-column window in registers,
+// waves unrolled in blocks of KR+1 so the window slots are compile-time (slot = column
+// mod (KR+1), the same register residency as the pipeline kernel): every panel element is
+// loaded and stored once per call.
+// ------------------------------------------------------------------------------------
+constexpr int kWaveChunkBlocks = 16;
+template <typename T, int KR, bool STRICT, bool REFL>
+__global__ void __launch_bounds__(128) rs_wave_kernel(T* __restrict__ P, long long m_r, long long ld,
+                                                      const T* __restrict__ ct, const T* __restrict__ st,
+                                                      long long n_waves, long long col0) {
+  constexpr int M = KR + 1;
+  constexpr int CHW = kWaveChunkBlocks * M;  // waves per staged chunk (a multiple of M)
+  extern __shared__ __align__(16) unsigned char wave_smem[];
+  T* const sc = reinterpret_cast<T*>(wave_smem);
+  T* const ss = sc + CHW * KR;
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = row < m_r;
+  T* const pr = P + (ok ? row : 0) + col0 * ld;
+  T win[M];
+  // at the start of wave w the window holds columns [w-1, w+KR-1]; column w+KR enters
+#pragma unroll
+  for (int c = 0; c < M; ++c) win[c] = (c < KR && ok) ? pr[c * ld] : T(0);
+  for (long long w0 = 0; w0 < n_waves; w0 += CHW) {
+    const long long nw = n_waves - w0 < CHW ? n_waves - w0 : CHW;
+    __syncthreads();
+    for (long long i = threadIdx.x; i < nw * KR; i += blockDim.x) {
+      sc[i] = ct[w0 * KR + i];
+      ss[i] = st[w0 * KR + i];
+    }
+    __syncthreads();
+    for (long long wb = 0; wb < nw; wb += M) {
+#pragma unroll
+      for (int u = 0; u < M; ++u) {
+        const long long w = w0 + wb + u;  // (w0 + wb) % M == 0: slot of column w is u
+        if (w < n_waves) {
+          win[(u + KR) % M] = ok ? pr[(w + KR) * ld] : T(0);
+#pragma unroll
+          for (int l = 0; l < KR; ++l) {
+            const T c = sc[(wb + u) * KR + l];
+            const T s = ss[(wb + u) * KR + l];
+            T& x = win[(u + KR - 1 - l) % M];
+            T& y = win[(u + KR - l) % M];
+            if constexpr (REFL) {
+              refl2<T, STRICT>(x, y, s, sub_rn(c, s), add_rn(c, s));
+            } else {
+              rot2<T, STRICT>(x, y, c, s);
+            }
+          }
+          // column w is final after wave w (its last transform is lane KR-1's x)
+          if (ok) pr[w * ld] = win[u];
+        }
+      }
+    }
+  }
+  // the columns still in the window, [n_waves, n_waves + KR), go back too
+  if (ok) {
+    const int base = (int)(n_waves % M);
+#pragma unroll
+    for (int sl = 0; sl < M; ++sl) {
+      const long long col = n_waves + (sl - base + M) % M;
+      if (col < n_waves + KR) pr[col * ld] = win[sl];
+    }
+  }
+}
+// wider waves (KR > 8): the same schedule with the window in L1 (global loads/stores)
+template <typename T, bool STRICT, bool REFL>
+__global__ void __launch_bounds__(128) rs_wave_kernel_wide(T* __restrict__ P, long long m_r, long long ld,
+                                                           const T* __restrict__ ct, const T* __restrict__ st,
+                                                           long long n_waves, int k_r, long long col0) {
+  const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= m_r) return;
+  T* const pr = P + row + col0 * ld;
+  for (long long w = 0; w < n_waves; ++w) {
+    for (int l = 0; l < k_r; ++l) {
+      const long long j = w + k_r - 1 - l;
+      const T c = __ldg(ct + w * k_r + l), s = __ldg(st + w * k_r + l);
+      T x = pr[j * ld], y = pr[(j + 1) * ld];
+      if constexpr (REFL) {
+        refl2<T, STRICT>(x, y, s, sub_rn(c, s), add_rn(c, s));
+      } else {
+        rot2<T, STRICT>(x, y, c, s);
+      }
+      pr[j * ld] = x;
+      pr[(j + 1) * ld] = y;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // FMA-pipe peak probe (roofline denominator: MEASURED_PEAKS.json has no FP64/FP32 entry)
 // ------------------------------------------------------------------------------------
 template <typename T>
@@ -1658,7 +1789,7 @@ __global__ void __launch_bounds__(256) rs_fma_peak_kernel(T* out, int iters, T a
 
 // Launches the pipeline kernel family <T, STRICT, REFL, HS> (defined and explicitly
 // instantiated in pipeline_variant.cu, one translation unit per family).
-template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT>
+template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT, int K>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P);
 
 }  // namespace rsk

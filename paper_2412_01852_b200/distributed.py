@@ -32,13 +32,30 @@ def owner_shard(total_owners: int, world: int, rank: int):
     return shard_range(total_owners, world, rank, align=TILE_OWNERS)
 
 
+def _dense_view(X):
+    """A contiguous view of X's storage (X itself, or its transpose for the column-major
+    C/S the library uses), or None when X is not dense in either order."""
+    if X.is_contiguous():
+        return X
+    if X.dim() == 2 and X.t().is_contiguous():
+        return X.t()
+    return None
+
+
 def broadcast_sequence(C, S, src: int = 0, group=None):
-    """Broadcast rank ``src``'s C and S (torch tensors of identical shape/dtype on
-    every rank; contents only matter on src) in place; returns (C, S)."""
+    """Broadcast rank ``src``'s C and S (torch tensors of identical shape, dtype and
+    strides on every rank; contents only matter on src) in place; returns (C, S).
+    Column-major C/S are sent as their dense storage (NCCL needs contiguous buffers)."""
     import torch.distributed as dist  # noqa: PLC0415
 
-    dist.broadcast(C, src=src, group=group)
-    dist.broadcast(S, src=src, group=group)
+    for X in (C, S):
+        view = _dense_view(X)
+        if view is not None:
+            dist.broadcast(view, src=src, group=group)
+        else:
+            tmp = X.contiguous()
+            dist.broadcast(tmp, src=src, group=group)
+            X.copy_(tmp)
     return C, S
 
 
