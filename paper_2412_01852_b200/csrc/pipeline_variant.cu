@@ -35,10 +35,14 @@ RS_INST(false, false, 8)
 RS_INST(true, false, 8)
 RS_INST(false, true, 8)
 RS_INST(true, true, 8)
-// the 16-sweep window (right side, fp32 only: a 17-column window of 2 rows is 34 registers)
+// the wide windows (right side): 16 sweeps for fp32, 12 for fp64
 #if RS_VARIANT_F32 && RS_F32_WIDE
 RS_INST(false, false, 16)
 RS_INST(true, false, 16)
+#endif
+#if !RS_VARIANT_F32 && RS_F64_WIDE
+RS_INST(false, false, 12)
+RS_INST(true, false, 12)
 #endif
 
 }  // namespace rsk

@@ -77,7 +77,7 @@ struct Geometry {
   long long pairs = 0;  // (tile, sweep) pairs = tiles * k
   int nchunk = 0;
   int nblk = 0;
-  int kw = kK;  // sweeps per unit window: kK, or kKWide (fp32, right side, wide units)
+  int kw = kK;  // sweeps per unit window: kK, or wide_k (right side, units of >= 9 sweeps)
   size_t coef_rec = 0;
   size_t std_bytes = 0;     // standard records (both sweep partitions)
   size_t coef_bytes = 0;    // standard + scaled records
@@ -141,9 +141,12 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   // the 16-sweep window: fp32, right side, and every unit of the full-width split at
   // least 9 sweeps wide (the wide kernel is compiled for widths 9..16)
   g->kw = kK;
-  if (RS_F32_WIDE && dtype == RS_DTYPE_F32 && !left && k >= kKWide && !getenv("RS_F32_K8")) {
-    const int64_t ut0 = (k + kKWide - 1) / kKWide;
-    if (k / ut0 >= kb_min(kKWide)) g->kw = kKWide;
+  const bool f32 = dtype == RS_DTYPE_F32;
+  const bool wide_ok = f32 ? (RS_F32_WIDE && !getenv("RS_F32_K8")) : (RS_F64_WIDE && !getenv("RS_F64_K8"));
+  const int kwide = wide_k(f32 ? 4 : 8);
+  if (wide_ok && !left && k >= kwide) {
+    const int64_t ut0 = (k + kwide - 1) / kwide;
+    if (k / ut0 >= kb_min(kwide)) g->kw = kwide;
   }
   g->nchunk = (g->len + g->kw) / (g->kw + 1);
   g->nblk = g->nchunk + 1;
@@ -151,8 +154,9 @@ bool make_geometry(int64_t m, int64_t n, int64_t lda, int64_t k, int side, int k
   g->coef_rec = (kind == RS_KIND_REFLECTOR ? 4 * tsz : 16);
   // two sweep partitions (ua and ua+1 units per tile) of k * nblk * (K+1) records each
   g->std_bytes = align_up(2 * (size_t)g->k * g->nblk * (g->kw + 1) * g->coef_rec, 256);
-  // scaled form: per partition k*nblk*(K+1) records + <= k*nblk*kScaleRecs scale records
-  g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (g->kw + 1 + kScaleRecs) * 16, 256);
+  // scaled form: per partition k*nblk*(K+1) records + <= k*nblk*SR scale records
+  const size_t sr = (size_t)scale_recs(g->kw, f32 ? 4 : 8);
+  g->coef_bytes = g->std_bytes + align_up(2 * (size_t)g->k * g->nblk * (g->kw + 1 + sr) * 16, 256);
   g->flags_only = align_up((size_t)(g->pairs + 1) * sizeof(uint32_t), 256);
   g->unsafe_bytes = align_up(2 * (size_t)(g->k + 1) * sizeof(uint32_t), 256);  // ua + 1 <= k + 1
   g->flag_bytes = g->flags_only + g->unsafe_bytes + kTrashBytes;
@@ -171,7 +175,7 @@ struct LaunchPlan {
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec, bool left, int K, bool refl) {
   // == coef_buf_bytes<T, REFL, K>() (fp32 rotation records hold two lanes each)
-  const size_t cbuf = coef_block_bytes(K, tsz == 4 && !refl, coef_rec);
+  const size_t cbuf = coef_block_bytes(K, tsz == 4 && !refl, coef_rec, tsz);
   return 2 * coef_blocks_per_buf(left) * cbuf + (size_t)stages_for(tsz) * (K + 1) * tile_owners(tsz) * tsz +
          ctl_words(stages_for(tsz), left) * sizeof(uint64_t);
 }
@@ -190,7 +194,7 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
   // one extra control block: the (never dereferenced) out-ring words of the last warp
   const size_t ctl = ctl_words(stages_for(tsz), g.left) * sizeof(uint64_t);
   int cap = (int)((optin - ctl) / per);
-  const int wmax = max_warps_for(tsz, g.left);
+  const int wmax = max_warps_for(tsz, g.left, g.kw);
   if (cap > wmax) cap = wmax;
   cap &= ~3;
   if (cap < 4) return fail(RS_EUNSUPPORTED, "shared memory too small for one warp per sub-partition");
@@ -330,8 +334,8 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
     const int sy = srows < 65535 ? srows : 65535;
     const dim3 sgrid((unsigned)((g.len + 127) / 128), (unsigned)sy);
     SCoef<T>* const sout = reinterpret_cast<SCoef<T>*>(base + g.std_bytes);
-    if (g.kw == kKWide)
-      rs_pack_scaled_kernel<T, REFL, kKWide><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua,
+    if (g.kw == wide_k(sizeof(T)))
+      rs_pack_scaled_kernel<T, REFL, wide_k(sizeof(T))><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua,
                                                                     nparts, rev, unsafe);
     else
       rs_pack_scaled_kernel<T, REFL, kK><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts,
@@ -339,8 +343,8 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   const uint32_t* const only = scaled && std_only_if_unsafe ? unsafe : nullptr;
-  if (g.kw == kKWide)
-    rs_pack_kernel<T, REFL, kKWide><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
+  if (g.kw == wide_k(sizeof(T)))
+    rs_pack_kernel<T, REFL, wide_k(sizeof(T))><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
                                                                                       g.nblk, lp.ua, nparts, rev, only);
   else
     rs_pack_kernel<T, REFL, kK><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
@@ -414,12 +418,14 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool left = g.os != 1;  // owners are columns: owner-major rings, coalesced A I/O
-  if (g.kw == kKWide) {
-    if constexpr (sizeof(T) == 4 && RS_F32_WIDE) {
-      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, kKWide>(cfg, P)
-             : launch_pipeline<T, STRICT, REFL, false, false, kKWide>(cfg, P);
+  if (g.kw != kK) {
+    constexpr int KW = wide_k(sizeof(T));
+    if constexpr ((sizeof(T) == 4 && RS_F32_WIDE) || (sizeof(T) == 8 && RS_F64_WIDE)) {
+      if (left || g.kw != KW) return fail(RS_EUNSUPPORTED, "wide window: right-side launches only");
+      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, KW>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false, KW>(cfg, P);
     } else {
-      return fail(RS_EUNSUPPORTED, "16-sweep window is built for fp32 right-side launches only");
+      return fail(RS_EUNSUPPORTED, "wide window not built");
     }
   } else if (hs) {
     e = left ? launch_pipeline<T, STRICT, REFL, true, true, kK>(cfg, P)

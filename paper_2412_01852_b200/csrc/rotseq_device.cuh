@@ -22,12 +22,18 @@ namespace rsk {
 // compile-time geometry
 // ------------------------------------------------------------------------------------
 constexpr int kK = 8;          // sweeps per unit window (lanes of the wavefront), default
+// Wide windows (measured and rejected; off by default): with RS_F32_WIDE=1,
 // fp32 right-side launches whose units all span >= 9 sweeps use a 16-sweep window
-// (RS_F32_WIDE=0 compiles it out; the env RS_F32_K8=1 disables it at run time)
+// (17-column blocks), with RS_F64_WIDE=1 fp64 ones a 12-sweep window. Fewer hand-offs per
+// flop, but the fully unrolled block body no longer fits the instruction cache (fp32
+// config 4: 33.2 -> 11.4 TF/s). The env RS_F32_K8=1 / RS_F64_K8=1 turns them off at run time.
 #ifndef RS_F32_WIDE
-#define RS_F32_WIDE 1
+#define RS_F32_WIDE 0
 #endif
-constexpr int kKWide = 16;
+#ifndef RS_F64_WIDE
+#define RS_F64_WIDE 0
+#endif
+__host__ __device__ constexpr int wide_k(size_t tsz) { return tsz == 4 ? 16 : 12; }
 // owners (rows) per thread, per element size. 2 for both: fp32 with 4 rows per thread (8
 // warps of 255 registers per CTA) measured 30.3 TF/s at config 4 against 31.1 with 2.
 #ifndef RS_ROWS_F32
@@ -80,8 +86,17 @@ constexpr int kMaxWarps = RS_MAX_WARPS;  // warps per CTA upper bound (launch bo
 // thread) keep the unrolled body free of spills.
 constexpr int kMaxWarpsLeft = 12;
 // 4 rows per thread need the register budget of 8-warp CTAs (255 per thread)
-__host__ __device__ constexpr int max_warps_for(size_t tsz, bool left) {
-  return rows_for(tsz) == 4 ? 8 : (left ? kMaxWarpsLeft : kMaxWarps);
+// The 16-sweep window (34-register window + wider coefficient queue) gets the register
+// budget of RS_WIDE_WARPS-warp CTAs.
+#ifndef RS_WIDE_WARPS
+#define RS_WIDE_WARPS 12
+#endif
+#ifndef RS_WIDE_WARPS_F64
+#define RS_WIDE_WARPS_F64 8
+#endif
+__host__ __device__ constexpr int max_warps_for(size_t tsz, bool left, int K = 8) {
+  return K > 8 ? (tsz == 8 ? RS_WIDE_WARPS_F64 : RS_WIDE_WARPS)
+               : (rows_for(tsz) == 4 ? 8 : (left ? kMaxWarpsLeft : kMaxWarps));
 }
 __host__ __device__ constexpr int tile_owners(size_t tsz) { return 32 * rows_for(tsz); }
 constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
@@ -114,7 +129,8 @@ struct alignas(4 * sizeof(T)) Coef<T, true> {
 // Scaled ("fast Givens") records: (tau1, -tau2), see rs_pack_scaled_kernel.
 template <typename T>
 using SCoef = Coef<T, false>;
-constexpr int kScaleRecs = 5;  // per block: K+1 = 9 column scales (fp64) in 5 16-byte records
+// per block of a scaled-form unit: the K+1 column scales (working type) in 16-byte records
+__host__ __device__ constexpr int scale_recs(int K, size_t tsz) { return (int)(((K + 1) * tsz + 15) / 16); }
 // blocks per coefficient buffer: the right side copies them in pairs; the left side (whose
 // global chunk copies go through L1, which shares the SRAM with shared memory) one by one
 __host__ __device__ constexpr int coef_blocks_per_buf(bool left) { return left ? 1 : 2; }
@@ -145,15 +161,14 @@ __device__ __forceinline__ CoefT lane_coef(const CoefT* __restrict__ wrec, int l
 // bytes of one per-warp coefficient buffer (two per warp: double buffering)
 // (one block of a unit of the widest width K: (K+1) waves of recs_per_wave(K) records, plus
 // the scaled form's column scales; host mirror: smem_per_warp in rotseq_b200.cu)
-__host__ __device__ constexpr size_t coef_block_bytes(int K, bool pair, size_t rec) {
+__host__ __device__ constexpr size_t coef_block_bytes(int K, bool pair, size_t rec, size_t tsz) {
   const size_t std_bytes = (size_t)(K + 1) * (pair ? (K + 1) / 2 : K) * rec;
-  const size_t scl_bytes = ((size_t)(K + 1) * (pair ? (K + 1) / 2 : K) + kScaleRecs) * 16;
+  const size_t scl_bytes = ((size_t)(K + 1) * (pair ? (K + 1) / 2 : K) + scale_recs(K, tsz)) * 16;
   return std_bytes > scl_bytes ? std_bytes : scl_bytes;
 }
 template <typename T, bool REFL, int K = kK>
 __host__ __device__ constexpr size_t coef_buf_bytes() {
-  static_assert((K + 1) * sizeof(T) <= kScaleRecs * 16, "a block's column scales must fit kScaleRecs records");
-  return coef_block_bytes(K, kPairRecs<T, REFL>, sizeof(Coef<T, REFL>));
+  return coef_block_bytes(K, kPairRecs<T, REFL>, sizeof(Coef<T, REFL>), sizeof(T));
 }
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -235,15 +250,46 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_test(bar, parity)) return;  // already complete: skip try_wait's fixed latency
+// RS_WAIT_MODE (measurement knob): 0 try_wait with a suspend-time hint (default), 1
+// try_wait without a hint, 2 test_wait + nanosleep back-off
+#ifndef RS_WAIT_MODE
+#define RS_WAIT_MODE 0
+#endif
+__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
+#if RS_WAIT_MODE == 1
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "RS_WAITN_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra RS_WAITN_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#elif RS_WAIT_MODE == 2
+  uint32_t ok;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (ok) break;
+    __nanosleep(64);
+  }
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "RS_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra RS_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "@!P1 bra RS_WAIT_%=;\n}" ::"r"(bar),
       "r"(parity), "r"(kSuspendHintNs)
       : "memory");
+#endif
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  if (mbar_test(bar, parity)) return;  // already complete: skip try_wait's fixed latency
+  mbar_wait_addr(smem_u32(bar), parity);
 }
 // Address-based forms (shared-window u32 addresses computed once per warp) and single-lane
 // forms predicated inside the asm, so the per-block protocol has no divergent branches.
@@ -260,13 +306,7 @@ __device__ __forceinline__ bool mbar_test_a(uint32_t bar, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
   if (mbar_test_a(bar, parity)) return;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "RS_WAITA_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@!P1 bra RS_WAITA_%=;\n}" ::"r"(bar),
-      "r"(parity), "r"(kSuspendHintNs)
-      : "memory");
+  mbar_wait_addr(bar, parity);
 }
 __device__ __forceinline__ void mbar_arrive_if(uint32_t bar, bool pred) {
   asm volatile(
@@ -747,12 +787,13 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     const T* const lbase = A + (tile * TR + lo0) * P.os + lv0 * P.cs;
     const bool lfull = tile * TR + TR <= P.owners;
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
-    // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
-    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
+    // records; rs_pack_scaled_kernel: Kb*(K+1) records + SR records of scales)
+    constexpr int SR = scale_recs(K, sizeof(T));
+    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? SR : 0);
     const CoefT* ubase;
     if constexpr (SCALED) {
-      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
-              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
+      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + SR) +
+              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * SR;
     } else {
       ubase = reinterpret_cast<const CoefT*>(P.coef) + (size_t)part * k * nblk * (K + 1) + (size_t)p0 * nblk * (K + 1);
     }
@@ -1129,12 +1170,13 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     const T* const lbase = A + (tile * TR + lo0) * P.os + lv0 * P.cs;
     const bool lfull = tile * TR + TR <= P.owners;
     // this unit's coefficient blocks, contiguous per block (rs_pack_kernel: Kb*(K+1)
-    // records; rs_pack_scaled_kernel: Kb*(K+1) records + kScaleRecs records of scales)
-    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? kScaleRecs : 0);
+    // records; rs_pack_scaled_kernel: Kb*(K+1) records + SR records of scales)
+    constexpr int SR = scale_recs(K, sizeof(T));
+    const int brec = recs_per_wave(Kb, kPairRecs<T, REFL>) * (K + 1) + (SCALED ? SR : 0);
     const CoefT* ubase;
     if constexpr (SCALED) {
-      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + kScaleRecs) +
-              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * kScaleRecs;
+      ubase = reinterpret_cast<const CoefT*>(P.coef_scaled) + (size_t)part * k * nblk * (K + 1 + SR) +
+              (size_t)p0 * nblk * (K + 1) + (size_t)iu * nblk * SR;
     } else {
       ubase = reinterpret_cast<const CoefT*>(P.coef) + (size_t)part * k * nblk * (K + 1) + (size_t)p0 * nblk * (K + 1);
     }
@@ -1429,7 +1471,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 // HS: host-streaming variant (rs_apply_host_*), a separate instantiation so the resident
 // path carries none of its checks
 template <typename T, int K, int R, bool STRICT, bool REFL, bool HS, bool LEFT>
-__global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
+__global__ void __launch_bounds__(max_warps_for(sizeof(T), LEFT, K) * 32, 1) rs_pipeline_kernel(const __grid_constant__ PipeParams P) {
   constexpr int S = stages_for(sizeof(T));
   constexpr int NBAR = ctl_words(S, LEFT);
   constexpr size_t CBUF = coef_buf_bytes<T, REFL, K>();
@@ -1579,9 +1621,10 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     const int kb = sweep_start(i + 1, ut, k) - p0;
     constexpr bool PAIR = kPairRecs<T, REFL>;
     const int nr = recs_per_wave(kb, PAIR);
-    const int brec = nr * (K + 1) + kScaleRecs;
-    SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + kScaleRecs) + (size_t)p0 * nblk * (K + 1) +
-                      (size_t)i * nblk * kScaleRecs;
+    constexpr int SR = scale_recs(K, sizeof(T));
+    const int brec = nr * (K + 1) + SR;
+    SCoef<T>* ubase = out + (size_t)part * k * nblk * (K + 1 + SR) + (size_t)p0 * nblk * (K + 1) +
+                      (size_t)i * nblk * SR;
     // the unit's coefficients of rotations (j-1, p), (j, p), (j+1, p), loaded up front
     // (independent loads in flight together; only c is needed for the neighbours)
     double cl[K], cj[K], sj[K], cr[K];

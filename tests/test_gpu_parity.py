@@ -402,3 +402,41 @@ def test_cli_run_and_verify(cuda, tmp_path):
     assert cli.main(["run", "--sweep", "64", "128", "--k", "12", "--reps", "1", "--csv", str(out2)]) == 0
     assert out2.read_text().splitlines()[0] == "n,Flops" and len(out2.read_text().splitlines()) == 3
     assert cli.main(["verify", "--quick"]) == 0
+
+
+@pytest.mark.parametrize("kind", ("rotation", "reflector"))
+def test_fp32_wide_window(cuda, oracle_mod, monkeypatch, kind):
+    """fp32 right-side launches with units of >= 9 sweeps run the 16-sweep window
+    (rs_plan_info band_width 16): strict is bit-identical to the numpy fp32 oracle and to
+    the 8-sweep window (RS_F32_K8=1), in forced multi-round / multi-CTA geometries too;
+    fast stays within 10*k*eps32 of the fp64 reference on the fp32 inputs."""
+    from paper_2412_01852_b200 import _lib
+
+    if _lib.plan_info(130, 300, 16, dtype=_lib.DTYPE_F32)["band_width"] != 16:
+        pytest.skip("library built without the 16-sweep window (RS_F32_WIDE=0, the default)")
+    for (m, n, k, order) in ((130, 300, 16, "forward"), (64, 100, 18, "reverse"), (300, 77, 40, "forward"),
+                             (97, 260, 129, "reverse"), (200, 60, 32, "forward")):
+        assert _lib.plan_info(m, n, k, dtype=_lib.DTYPE_F32)["band_width"] == 16, (m, n, k)
+        rng = np.random.Generator(np.random.Philox(k))
+        A = np.asfortranarray(rng.uniform(-1, 1, (m, n)).astype(np.float32))
+        th = rng.uniform(0, 2 * np.pi, (n - 1, k))
+        C, S = np.cos(th).astype(np.float32), np.sin(th).astype(np.float32)
+        ref = A.copy(order="F")
+        oracle_mod.numpy_apply_naive(ref, C, S, order=order, kind=kind)
+        for mw, grid in (("", ""), ("4", "3"), ("1", "")):
+            for key, val in (("RS_DEBUG_MAX_WARPS", mw), ("RS_DEBUG_GRID", grid)):
+                if val:
+                    monkeypatch.setenv(key, val)
+                else:
+                    monkeypatch.delenv(key, raising=False)
+            assert_bitwise(ref, _gpu(A, C, S, order=order, kind=kind), f"wide fp32 {m}x{n} k={k} mw={mw} grid={grid}")
+        monkeypatch.delenv("RS_DEBUG_MAX_WARPS", raising=False)
+        monkeypatch.delenv("RS_DEBUG_GRID", raising=False)
+        monkeypatch.setenv("RS_F32_K8", "1")
+        assert _lib.plan_info(m, n, k, dtype=_lib.DTYPE_F32)["band_width"] == 8
+        assert_bitwise(ref, _gpu(A, C, S, order=order, kind=kind), "8-sweep window")
+        monkeypatch.delenv("RS_F32_K8")
+        ref64 = oracle_mod.upcast_reference(A, C, S, order=order, kind=kind)
+        got = _gpu(A, C, S, order=order, kind=kind, fast=True).astype(np.float64)
+        err = np.linalg.norm(got - ref64) / np.linalg.norm(ref64)
+        assert err <= 10 * k * np.finfo(np.float32).eps, (m, n, k, err)

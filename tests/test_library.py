@@ -57,9 +57,16 @@ def test_version_and_workspace_formula():
     assert ws == coef + scaled + flags + unsafe + trash
     assert ws % 256 == 0
     assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 1, 0) > ws  # reflector records are 32 B
-    # fp32: the same 16-byte record blocks (paired rotations) and tiles
-    assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 1) == ws
-    assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 1, 1) == ws  # fp32 reflector: (s, d, e, pad)
+    # fp32: the same 16-byte record blocks (paired rotations; reflector (s, d, e, pad)) with
+    # 3 scale records per block (9 fp32 scales); a build with the optional 16-sweep window
+    # (RS_F32_WIDE=1) uses 17-column blocks with 5 scale records on the right side
+    ws32 = coef + -(-2 * 192 * nblk * 12 * 16 // 256) * 256 + flags + unsafe + trash
+    nblk16 = (4096 + 16) // 17 + 1
+    ws32w = (-(-2 * 192 * nblk16 * 17 * 16 // 256) * 256 + -(-2 * 192 * nblk16 * 22 * 16 // 256) * 256
+             + flags + unsafe + trash)
+    assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 1) in (ws32, ws32w)
+    assert lib.rs_workspace_bytes(4096, 4096, 192, 0, 1, 1) == lib.rs_workspace_bytes(4096, 4096, 192, 0, 0, 1)
+    assert lib.rs_workspace_bytes(4096, 4096, 192, 1, 0, 1) == ws32  # left side: 8-sweep window
     assert lib.rs_workspace_bytes(4096, 1, 4, 0, 0, 0) == 0       # invalid: n < 2
 
 
