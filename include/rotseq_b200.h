@@ -164,6 +164,18 @@ rs_status rs_wave_apply_f32(float* panel, int64_t m_r, int64_t n_cols, int64_t l
                             const float* st, int64_t n_waves, int64_t k_r, int64_t col0, int kind, int strict,
                             void* stream);
 
+/* The accumulate-and-apply variant on the FP64 tensor cores (the paper's rs_gemm,
+ * PAPER.md:860; explicit-Q idea of accumulate_q, oracle.py:102-109): the k sweeps in passes
+ * of 32, each pass's rotations grouped into 64 x 64 window products Q_w (32 waves each)
+ * that are applied as A[:, window] <- A[:, window] * Q_w with DMMA (mma.sync m8n8k4 f64).
+ * Right side, either order and kind, fp64, fast-mode accuracy (within the BASELINE
+ * tolerance, not bit-identical). Device pointers; asynchronous on `stream`; `workspace`
+ * (rs_dmma_workspace_bytes(), 256-byte aligned) may be NULL (stream-ordered allocation). */
+size_t rs_dmma_workspace_bytes(int64_t m, int64_t n, int64_t k);
+rs_status rs_apply_dmma_f64(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S,
+                            int64_t ldcs, int64_t k, int order, int kind, void* workspace, size_t workspace_bytes,
+                            void* stream);
+
 /* Launch geometry the pipeline would use for this problem on the current device
  * (for benchmarks / roofline accounting). Any out-pointer may be NULL. */
 rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int dtype,

@@ -32,6 +32,8 @@ from .apply import (  # noqa: F401
     apply_blocked,
     apply_cuda,
     apply_device,
+    apply_dmma,
+    dmma_workspace_bytes,
     apply_host,
     apply_naive,
     workspace_bytes,

@@ -50,6 +50,8 @@ EXPORTS = (
     "rs_apply_host_f32",
     "rs_wave_apply_f64",
     "rs_wave_apply_f32",
+    "rs_dmma_workspace_bytes",
+    "rs_apply_dmma_f64",
     "rs_launch_count",
     "rs_debug_set_trace",
     "rs_fma_peak_tflops",
@@ -63,7 +65,23 @@ class LibraryNotBuilt(RuntimeError):
     pass
 
 
+class _Partial:
+    """Developer builds selected with RS_LIB_PATH may predate newer entry points: declaring
+    a symbol they lack is skipped (calling it raises AttributeError)."""
+
+    def __init__(self, lib):
+        self._lib = lib
+
+    def __getattr__(self, name):
+        try:
+            return getattr(self._lib, name)
+        except AttributeError:
+            return type("_Missing", (), {})()
+
+
 def _declare(lib):
+    if os.environ.get("RS_LIB_PATH"):
+        lib = _Partial(lib)
     i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
     lib.rs_version.restype = i32
     lib.rs_version.argtypes = []
@@ -96,6 +114,10 @@ def _declare(lib):
         fn = getattr(lib, name)
         fn.restype = i32
         fn.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i64, i32, i32, vp]
+    lib.rs_dmma_workspace_bytes.restype = sz
+    lib.rs_dmma_workspace_bytes.argtypes = [i64, i64, i64]
+    lib.rs_apply_dmma_f64.restype = i32
+    lib.rs_apply_dmma_f64.argtypes = [vp, i64, i64, i64, vp, vp, i64, i64, i32, i32, vp, sz, vp]
     lib.rs_packed_form.restype = i32
     lib.rs_packed_form.argtypes = [vp, sz, i64, i64, i64, i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64), vp]
     lib.rs_plan_info.restype = i32
@@ -108,7 +130,7 @@ def _declare(lib):
     lib.rs_fma_peak_tflops.argtypes = [i32, ctypes.POINTER(ctypes.c_double), vp]
     lib.rs_debug_set_trace.restype = i32
     lib.rs_debug_set_trace.argtypes = [vp]
-    return lib
+    return lib._lib if isinstance(lib, _Partial) else lib
 
 
 def load():

@@ -432,3 +432,57 @@ class PackedSequence:
                     0 if fast else 1, self.workspace.data_ptr(), self.workspace.numel(), lstream.cuda_stream)
             _keep_alive(lstream, cur, self.workspace)
         _lib.check(st, "rs_apply_packed")
+
+
+def apply_dmma(A, seq, kind=TransformKind.ROTATION, order=Order.FORWARD, workspace=None, stream=None) -> None:
+    """The FP64 tensor-core (DMMA) accumulate-and-apply variant (``rs_apply_dmma_f64``;
+    the paper's rs_gemm): right side, fp64, fast-mode accuracy. ``A`` is a
+    column-major CUDA float64 tensor (updated in place on ``stream``) or a host array
+    (copied to the device and back)."""
+    torch = _torch()
+    kind = _as_enum(kind, TransformKind, "kind")
+    order = _as_enum(order, Order, "order")
+    if not (_is_tensor(A) and A.is_cuda):
+        check_apply_args(A, seq, Side.RIGHT)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        dA = _np_to_device(np.asarray(A), torch.float64, dev)
+        apply_dmma(dA, seq, kind, order, workspace, stream)
+        if isinstance(A, np.ndarray):
+            A[...] = dA.cpu().numpy()
+        else:
+            A.copy_(dA.cpu())
+        return
+    if A.dim() != 2 or A.dtype != torch.float64:
+        raise ValueError("the DMMA variant needs a 2-D float64 matrix")
+    m, n = int(A.shape[0]), int(A.shape[1])
+    if m > 1 and A.stride(0) != 1:
+        raise ValueError("A must be column-major (first stride 1)")
+    if n < 2:
+        raise ValueError(f"matrix needs at least 2 columns, got {n}")
+    ncols = _seq_ncols(seq)
+    if ncols != n:
+        raise ValueError(f"sequence acts on {ncols} columns but matrix has {n}")
+    if m == 0:
+        return
+    C, S = _seq_arrays(seq, torch.float64, A.device)
+    rows_cs, k = int(C.shape[0]), int(C.shape[1])
+    if not all(X.shape[0] <= 1 or X.stride(0) == 1 for X in (C, S)) or C.stride(1) != S.stride(1):
+        C, S = C.t().contiguous().t(), S.t().contiguous().t()
+    ldcs = int(C.stride(1)) if k > 1 else max(rows_cs, 1)
+    lda = int(A.stride(1)) if n > 1 else max(m, 1)
+    lib = _lib.load()
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    with torch.cuda.device(A.device):
+        lstream, cur = _launch_stream(stream, A.device)
+        st = lib.rs_apply_dmma_f64(A.data_ptr(), m, n, lda, C.data_ptr(), S.data_ptr(), ldcs, k,
+                                   _lib.ORDER_REVERSE if order is Order.REVERSE else _lib.ORDER_FORWARD,
+                                   _lib.KIND_REFLECTOR if kind is TransformKind.REFLECTOR else _lib.KIND_ROTATION,
+                                   ws_ptr, ws_bytes, lstream.cuda_stream)
+        _keep_alive(lstream, cur, C, S)
+    _lib.check(st, "rs_apply_dmma")
+
+
+def dmma_workspace_bytes(m: int, n: int, k: int) -> int:
+    return int(_lib.load().rs_dmma_workspace_bytes(m, n, k))

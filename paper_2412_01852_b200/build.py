@@ -8,7 +8,8 @@ Translation units (compiled in parallel, then linked with the static CUDA runtim
 
 * ``csrc/rotseq_b200.cu``       host side, C-ABI, pack / naive / peak kernels;
 * ``csrc/pipeline_variant.cu``  compiled 8 times, once per pipeline-kernel family
-  (fp64/fp32 x strict/fast x rotation/reflector).
+  (fp64/fp32 x strict/fast x rotation/reflector);
+* ``csrc/dmma_variant.cu``      the FP64 tensor-core accumulate-and-apply variant.
 """
 
 from __future__ import annotations
@@ -24,6 +25,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SRC = os.path.join(CSRC, "rotseq_b200.cu")
 VARIANT_SRC = os.path.join(CSRC, "pipeline_variant.cu")
+DMMA_SRC = os.path.join(CSRC, "dmma_variant.cu")
 DEVICE_HDR = os.path.join(CSRC, "rotseq_device.cuh")
 HDR = os.path.join(ROOT, "include", "rotseq_b200.h")
 OUT = os.path.join(HERE, "librotseq_b200.so")
@@ -59,7 +61,7 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
     """Compile (in parallel) and link the library. ``out``/``extra`` build developer
     variants (e.g. ``extra=["-DRS_TRACE"]``) without touching the product .so."""
     out = out or OUT
-    deps = [SRC, VARIANT_SRC, DEVICE_HDR, HDR, __file__]
+    deps = [SRC, VARIANT_SRC, DMMA_SRC, DEVICE_HDR, HDR, __file__]
     if not force and extra is None and not _stale(out, deps):
         return out
     extra = list(extra or []) + os.environ.get("RS_NVCC_EXTRA", "").split()
@@ -69,6 +71,8 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
     try:
         jobs = [(os.path.join(tmpdir, "host.o"), [nvcc, *NVCC_FLAGS, *extra, *inc, "-c", "-o",
                                                    os.path.join(tmpdir, "host.o"), SRC])]
+        jobs.append((os.path.join(tmpdir, "dmma.o"), [nvcc, *NVCC_FLAGS, *extra, *inc, "-c", "-o",
+                                                      os.path.join(tmpdir, "dmma.o"), DMMA_SRC]))
         for t, s, r in VARIANTS:
             obj = os.path.join(tmpdir, f"pipe_{t}_{s}_{r}.o")
             jobs.append((obj, [nvcc, *NVCC_FLAGS, *extra, *inc, f"-DRS_VARIANT_T={t}", f"-DRS_VARIANT_STRICT={s}",

@@ -52,6 +52,13 @@
 
 #define RS_VERSION 10300
 
+namespace rsk {
+// the FP64 tensor-core variant (dmma_variant.cu)
+size_t dmma_workspace(int64_t m, int64_t n, int64_t k);
+int dmma_run(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S, int64_t ldcs,
+             int64_t k, int rev, int refl, void* workspace, cudaStream_t st);
+}  // namespace rsk
+
 namespace {
 
 using namespace rsk;
@@ -1131,6 +1138,46 @@ rs_status rs_wave_apply_f32(float* panel, int64_t m_r, int64_t n_cols, int64_t l
                             void* stream) {
   g_err.clear();
   return wave_impl<float>(panel, m_r, n_cols, ld, ct, st, n_waves, k_r, col0, kind, strict, stream);
+}
+
+size_t rs_dmma_workspace_bytes(int64_t m, int64_t n, int64_t k) { return dmma_workspace(m, n, k); }
+
+rs_status rs_apply_dmma_f64(double* A, int64_t m, int64_t n, int64_t lda, const double* C, const double* S,
+                            int64_t ldcs, int64_t k, int order, int kind, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  g_err.clear();
+  if (order != RS_ORDER_FORWARD && order != RS_ORDER_REVERSE)
+    return fail(RS_EINVAL, "order must be 0 (forward) or 1 (reverse)");
+  if (kind != RS_KIND_ROTATION && kind != RS_KIND_REFLECTOR)
+    return fail(RS_EINVAL, "kind must be 0 (rotation) or 1 (reflector)");
+  if (m < 0 || n < 0) return fail(RS_EINVAL, "matrix dimensions must be non-negative");
+  if (n < 2) return fail(RS_EINVAL, "matrix needs at least 2 columns");
+  if (n > ((int64_t)1 << 26)) return fail(RS_EUNSUPPORTED, "rotated dimension longer than 2^26");
+  if (k < 1) return fail(RS_EINVAL, "need k >= 1 sequences");
+  if (k > ((int64_t)1 << 20)) return fail(RS_EUNSUPPORTED, "more than 2^20 sequences");
+  if (lda < (m > 1 ? m : 1)) return fail(RS_EINVAL, "lda must be >= max(1, m) (column-major)");
+  if (ldcs < n - 1) return fail(RS_EINVAL, "ldcs must be >= len - 1");
+  if (m == 0) return RS_OK;
+  if (!A || !C || !S) return fail(RS_EINVAL, "null pointer");
+  const size_t need = dmma_workspace(m, n, k);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  void* ws = workspace;
+  bool owned = false;
+  if (ws == nullptr) {
+    cudaError_t e = pool_alloc(&ws, need, st);
+    if (e != cudaSuccess) return fail(RS_ENOMEM, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    owned = true;
+  } else if (workspace_bytes < need) {
+    return fail(RS_ENOMEM, "workspace smaller than rs_dmma_workspace_bytes()");
+  } else if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) {
+    return fail(RS_EINVAL, "workspace must be 256-byte aligned");
+  }
+  const int launched = dmma_run(A, m, n, lda, C, S, ldcs, k, order == RS_ORDER_REVERSE,
+                                kind == RS_KIND_REFLECTOR, ws, st);
+  if (launched > 0) g_launches.fetch_add(launched, std::memory_order_relaxed);
+  if (owned) cudaFreeAsync(ws, st);
+  if (launched < 0) return fail(RS_ECUDA, std::string("dmma launch: ") + cudaGetErrorString(cudaGetLastError()));
+  return RS_OK;
 }
 
 rs_status rs_debug_set_trace(void* device_ptr) {

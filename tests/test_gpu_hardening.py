@@ -245,3 +245,30 @@ def test_cli_verify_and_fault_injection(cuda, capsys):
     err = capsys.readouterr().err
     assert "FIRST FAILURE cuda" in err
     assert os.environ.get("ROTSEQ_PERTURB_KERNEL") is None  # restored
+
+
+@pytest.mark.parametrize("kind", ["rotation", "reflector"])
+@pytest.mark.parametrize("order", ["forward", "reverse"])
+def test_dmma_variant_matches_oracle(cuda, oracle_mod, kind, order):
+    """The FP64 tensor-core variant (rs_apply_dmma_f64) against the strict oracle at
+    BASELINE's 10*k*eps: partial row tiles, partial passes (k not a multiple of 32),
+    windows clipped at both ends, odd lda views."""
+    import torch
+
+    from paper_2412_01852_b200 import apply_dmma, compare, make_inputs
+
+    for (m, n, k) in ((64, 64, 32), (100, 70, 40), (33, 300, 7), (257, 129, 65), (8, 2, 3)):
+        A0, seq = make_inputs(m, n, k, 13)
+        ref = A0.copy(order="F")
+        oracle_mod.apply_naive(ref, seq.C, seq.S, order=order, kind=kind)
+        got = A0.copy(order="F")
+        apply_dmma(got, seq, kind=kind, order=order)
+        rep = compare(ref, got, "baseline", k=k)
+        assert rep.passed, f"{m}x{n} k={k}: {rep}"
+        # a row-block view with odd lda on the device
+        big = torch.zeros((n, m + 3), dtype=torch.float64, device="cuda").t()
+        view = big[1:m + 1, :]
+        view.copy_(torch.from_numpy(A0))
+        apply_dmma(view, seq, kind=kind, order=order)
+        rep = compare(ref, view.cpu().numpy(), "baseline", k=k)
+        assert rep.passed, f"view {m}x{n} k={k}: {rep}"
