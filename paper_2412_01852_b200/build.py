@@ -14,6 +14,7 @@ Translation units (compiled in parallel, then linked with the static CUDA runtim
 
 from __future__ import annotations
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -57,9 +58,23 @@ def _run(cmd):
     return proc.stderr
 
 
+OBJ_CACHE = os.path.join(ROOT, "build", "obj")  # git-ignored: per-TU objects keyed by content
+
+
+def _key(cmd, sources) -> str:
+    h = hashlib.sha1(" ".join(cmd).encode())
+    for src in sources:
+        with open(src, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
 def build_library(force: bool = False, verbose: bool = False, out: str | None = None, extra=None) -> str:
     """Compile (in parallel) and link the library. ``out``/``extra`` build developer
-    variants (e.g. ``extra=["-DRS_TRACE"]``) without touching the product .so."""
+    variants (e.g. ``extra=["-DRS_TRACE"]``) without touching the product .so. Objects are
+    cached per translation unit under build/obj, keyed by the compile command and the
+    contents of the sources it includes, so an edit recompiles only what it touches
+    (``force`` only forces the link)."""
     out = out or OUT
     deps = [SRC, VARIANT_SRC, DMMA_SRC, DEVICE_HDR, HDR, __file__]
     if not force and extra is None and not _stale(out, deps):
@@ -67,25 +82,43 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
     extra = list(extra or []) + os.environ.get("RS_NVCC_EXTRA", "").split()
     nvcc = nvcc_path()
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
-    tmpdir = tempfile.mkdtemp(prefix="rs_build_", dir=HERE)
+    os.makedirs(OBJ_CACHE, exist_ok=True)
+    units = [("host", [], SRC, [SRC, DEVICE_HDR, HDR]), ("dmma", [], DMMA_SRC, [DMMA_SRC, DEVICE_HDR, HDR])]
+    for t, s, r in VARIANTS:
+        units.append((f"pipe_{t}_{s}_{r}", [f"-DRS_VARIANT_T={t}", f"-DRS_VARIANT_STRICT={s}", f"-DRS_VARIANT_REFL={r}",
+                                             f"-DRS_VARIANT_F32={int(t == 'float')}"], VARIANT_SRC,
+                      [VARIANT_SRC, DEVICE_HDR, HDR]))
+    jobs = []
+    for name, defs, src, srcdeps in units:
+        base = [nvcc, *NVCC_FLAGS, *extra, *inc, *defs]
+        obj = os.path.join(OBJ_CACHE, f"{name}-{_key(base + [src], srcdeps)}.o")
+        jobs.append((obj, base + ["-c", "-o", obj + ".tmp", src]))
+    todo = [j for j in jobs if not os.path.exists(j[0])]
+
+    def compile_one(job):
+        log = _run(job[1])
+        os.replace(job[0] + ".tmp", job[0])
+        with open(job[0] + ".log", "w") as fh:
+            fh.write(log)
+        return log
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo) or 1, os.cpu_count() or 1))) as pool:
+        list(pool.map(compile_one, todo))
+    logs = []
+    for obj, _ in jobs:
+        try:
+            with open(obj + ".log") as fh:
+                logs.append(fh.read())
+        except OSError:
+            pass
+    fd, tmp = tempfile.mkstemp(suffix=".so", dir=os.path.dirname(out))
+    os.close(fd)
     try:
-        jobs = [(os.path.join(tmpdir, "host.o"), [nvcc, *NVCC_FLAGS, *extra, *inc, "-c", "-o",
-                                                   os.path.join(tmpdir, "host.o"), SRC])]
-        jobs.append((os.path.join(tmpdir, "dmma.o"), [nvcc, *NVCC_FLAGS, *extra, *inc, "-c", "-o",
-                                                      os.path.join(tmpdir, "dmma.o"), DMMA_SRC]))
-        for t, s, r in VARIANTS:
-            obj = os.path.join(tmpdir, f"pipe_{t}_{s}_{r}.o")
-            jobs.append((obj, [nvcc, *NVCC_FLAGS, *extra, *inc, f"-DRS_VARIANT_T={t}", f"-DRS_VARIANT_STRICT={s}",
-                               f"-DRS_VARIANT_REFL={r}", f"-DRS_VARIANT_F32={int(t == 'float')}", "-c", "-o", obj,
-                               VARIANT_SRC]))
-        with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as pool:
-            logs = list(pool.map(lambda j: _run(j[1]), jobs))
-        fd, tmp = tempfile.mkstemp(suffix=".so", dir=os.path.dirname(out))
-        os.close(fd)
         _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *[j[0] for j in jobs]])
         os.replace(tmp, out)
     finally:
-        shutil.rmtree(tmpdir, ignore_errors=True)
+        if os.path.exists(tmp):
+            os.remove(tmp)
     info = "\n".join(logs)
     if verbose:
         print(info)

@@ -12,8 +12,9 @@
 // the plain loop up to rounding). Q_w is built once per call (rs_dmma_q_kernel: 64 threads,
 // thread i carries row i of Q through the window's rotations in the reference's order) and
 // applied with mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4) by rs_dmma_apply_kernel: a CTA owns 32
-// rows of A and streams the windows, keeping the 64 window columns in a 96-column shared
-// ring (the next 32 columns prefetched by cp.async while the current window multiplies),
+// rows of A and streams the windows, the 64 window columns in shared memory (32 carried
+// from the previous window, 32 new ones prefetched by cp.async while the current window
+// multiplies),
 // Q_w double-buffered by a TMA bulk copy, and 8x8 tiles of Q_w that are structurally zero
 // (the parallelogram's corners: 12 of 64 tiles) skipped.
 //
@@ -38,47 +39,73 @@ constexpr int kDKB = 32;               // sweeps per pass
 constexpr int kDW = kDNB + kDKB;       // window columns (64)
 constexpr int kDRows = 32;             // rows of A per CTA
 constexpr int kDColStride = kDRows + 4;  // shared column stride (doubles): conflict-free A fragments
-constexpr int kDRing = 3 * 32;         // shared column ring (3 groups of 32)
 constexpr int kDQ = kDW * kDW;         // doubles per Q_w
 
 __host__ __device__ inline int dmma_windows(int n) { return (n + kDKB - 2 + kDNB - 1) / kDNB; }
 
-// Q_w for (pass, window) = (blockIdx.y, blockIdx.x). Thread i keeps row i of Q in shared
-// memory and applies the window's rotations in wave order, lanes ascending (column
-// operations Q <- Q * G, as accumulate_q does). Output in DMMA B-fragment order:
-// Qf[(ks * 8 + nt) * 32 + lane] = Q[ks*4 + lane%4][nt*8 + lane/4]; plus a 64-bit mask of the
-// nonzero 8x8 tiles (bit kt*8 + nt).
+// Q_w for (pass, window) = (blockIdx.y, blockIdx.x). The window's coefficients (rotation
+// pairs j in [c0, c0 + 62], the pass's lanes) are staged in shared memory first, then thread
+// i keeps row i of Q in registers and applies the window's rotations in wave order, lanes
+// ascending (column operations Q <- Q * G, as accumulate_q does). Output in DMMA
+// B-fragment order: Qf[(ks * 8 + nt) * 32 + lane] = Q[ks*4 + lane%4][nt*8 + lane/4]; plus a
+// 64-bit mask of the nonzero 8x8 tiles (bit kt*8 + nt).
+constexpr int kDPairs = kDW - 1;  // rotation pairs a window can touch (63)
 template <bool REFL>
 __global__ void __launch_bounds__(kDW) rs_dmma_q_kernel(double* __restrict__ qout, unsigned long long* __restrict__ masks,
                                                         const double* __restrict__ C, const double* __restrict__ S,
                                                         long long ldcs, int n, int k, int rev) {
-  __shared__ double q[kDW][kDW + 1];
+  extern __shared__ __align__(16) unsigned char qsm[];
+  double2 (*cs)[kDPairs] = reinterpret_cast<double2 (*)[kDPairs]>(qsm);  // (c, s) of pair c0 + x, lane l
   __shared__ unsigned long long tile_bits[kDW];
   const int i = threadIdx.x;
   const int w = blockIdx.x, pass = blockIdx.y;
   const int p0 = pass * kDKB;
   const int lanes = k - p0 < kDKB ? k - p0 : kDKB;
-#pragma unroll 8
-  for (int c = 0; c < kDW; ++c) q[i][c] = c == i ? 1.0 : 0.0;
   const int c0 = w * kDNB - kDKB + 1;
-  for (int t = w * kDNB; t < (w + 1) * kDNB; ++t) {
-    for (int l = 0; l < lanes; ++l) {
-      const int j = t - l;
-      if (j < 0 || j > n - 2) continue;
+  // pairs outside the matrix and lanes past the pass are staged as identities (c, s) = (1, 0):
+  // the rotation loop below then needs no predicates (an identity is exact)
+  for (int e = i; e < kDKB * kDPairs; e += kDW) {
+    const int l = e / kDPairs, x = e - l * kDPairs;
+    const int j = c0 + x;
+    double c = 1.0, s = 0.0;
+    bool id = true;
+    if (l < lanes && j >= 0 && j <= n - 2) {
       const long long jj = rev ? (long long)(n - 2 - j) : (long long)j;
-      double c = __ldg(C + jj + (long long)(p0 + l) * ldcs);
-      double s = __ldg(S + jj + (long long)(p0 + l) * ldcs);
-      const int x = j - c0;
-      const double qx = q[i][x], qy = q[i][x + 1];
+      c = __ldg(C + jj + (long long)(p0 + l) * ldcs);
+      s = __ldg(S + jj + (long long)(p0 + l) * ldcs);
+      if (rev) {
+        if constexpr (REFL) c = -c; else s = -s;
+      }
+      id = false;
+    }
+    if constexpr (REFL) {
+      // a reflector is not an identity for any (c, s): mark skipped pairs with s = NaN
+      if (id) s = __longlong_as_double(0x7ff8000000000001ll);
+    }
+    cs[l][x] = make_double2(c, s);
+  }
+  __syncthreads();
+  // row i of Q in registers: column x of the window is q[x] (compile-time indices: the
+  // wave and lane loops are fully unrolled, x = (t - 32 w) + 31 - l)
+  double q[kDW];
+#pragma unroll
+  for (int c = 0; c < kDW; ++c) q[c] = c == i ? 1.0 : 0.0;
+#pragma unroll
+  for (int tt = 0; tt < kDNB; ++tt) {
+#pragma unroll
+    for (int l = 0; l < kDKB; ++l) {
+      const int x = tt + kDKB - 1 - l;
+      const double2 r = cs[l][x];
+      const double qx = q[x], qy = q[x + 1];
       if constexpr (REFL) {
-        if (rev) c = -c;
-        const double w2 = s * (qx + qy);
-        q[i][x] = fma(c - s, qx, w2);
-        q[i][x + 1] = fma(-(c + s), qy, w2);
+        if (r.y == r.y) {  // not a skipped pair (NaN marker)
+          const double w2 = r.y * (qx + qy);
+          q[x] = fma(r.x - r.y, qx, w2);
+          q[x + 1] = fma(-(r.x + r.y), qy, w2);
+        }
       } else {
-        if (rev) s = -s;
-        q[i][x] = fma(s, qy, c * qx);
-        q[i][x + 1] = fma(c, qy, -s * qx);
+        q[x] = fma(r.y, qy, r.x * qx);
+        q[x + 1] = fma(r.x, qy, -r.y * qx);
       }
     }
   }
@@ -86,11 +113,10 @@ __global__ void __launch_bounds__(kDW) rs_dmma_q_kernel(double* __restrict__ qou
   double* const qw = qout + ((size_t)pass * gridDim.x + w) * kDQ;
   const int ks = i >> 2, lq = i & 3;
   unsigned long long bits = 0;
-#pragma unroll 8
+#pragma unroll
   for (int c = 0; c < kDW; ++c) {
-    const double v = q[i][c];
-    qw[(ks * 8 + (c >> 3)) * 32 + lq + 4 * (c & 7)] = v;
-    if (v != 0.0) bits |= 1ull << ((i >> 3) * 8 + (c >> 3));
+    qw[(ks * 8 + (c >> 3)) * 32 + lq + 4 * (c & 7)] = q[c];
+    if (q[c] != 0.0) bits |= 1ull << ((i >> 3) * 8 + (c >> 3));
   }
   tile_bits[i] = bits;
   __syncthreads();
@@ -103,19 +129,26 @@ __global__ void __launch_bounds__(kDW) rs_dmma_q_kernel(double* __restrict__ qou
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d[0]), "+d"(d[1])
-               : "d"(a), "d"(b));
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
 }
 
-// One pass over all windows for 32 rows of A (right side; A column-major, lda).
+// One pass over all windows for 32 rows of A (right side; A column-major, lda; a negative
+// lda walks the columns backwards for reverse order). Window w's 64 columns are its 32
+// carried columns (cbuf[(w+1)&1]: window w-1's outputs 32..63, already rotated by the
+// earlier windows of this pass) followed by 32 new columns from A (nbuf[w&1], prefetched by
+// cp.async one window ahead). Outputs 0..31 are final for the pass and go to A, outputs
+// 32..63 go to cbuf[w&1] for window w+1: one __syncthreads per window orders everything
+// (buffers alternate, so no window writes what the previous one may still read).
 __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restrict__ A, long long m, long long lda,
                                                                int n, const double* __restrict__ qpass,
                                                                const unsigned long long* __restrict__ mpass,
                                                                int nwin) {
   extern __shared__ __align__(128) unsigned char dsm[];
-  double* const qbuf = reinterpret_cast<double*>(dsm);                 // 2 x kDQ
-  double* const ring = qbuf + 2 * kDQ;                                 // kDRing x kDColStride
-  uint64_t* const qbar = reinterpret_cast<uint64_t*>(ring + kDRing * kDColStride);  // 2 mbarriers
+  double* const qbuf = reinterpret_cast<double*>(dsm);  // 2 x kDQ (TMA, double buffered)
+  double* const cbuf = qbuf + 2 * kDQ;                  // 2 x 32 columns x kDColStride (carried)
+  double* const nbuf = cbuf + 2 * 32 * kDColStride;     // 2 x 32 columns x kDColStride (new)
+  uint64_t* const qbar = reinterpret_cast<uint64_t*>(nbuf + 2 * 32 * kDColStride);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long r0 = (long long)blockIdx.x * kDRows;
   if (tid == 0) {
@@ -123,20 +156,17 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
     mbar_init(&qbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-  // column c of A lives in ring slot ((c + KB - 1) mod 96); a group of 32 columns starts at
-  // c0(w) + 32 g. Cooperative cp.async of group g (32 columns x 32 rows, one element per
-  // copy: any lda; columns or rows outside the matrix are zero-filled).
-  auto load_group = [&](int g) {
-    const int cbase = g * 32 - kDKB + 1;
+  // 32 columns starting at col0 into dst (one element per cp.async: any lda and alignment;
+  // columns or rows outside the matrix are zero-filled)
+  auto load_cols = [&](double* dst, int col0) {
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
-      const int idx = tid + it * 256;  // 1024 elements: column cl = idx / 32, row idx % 32
+      const int idx = tid + it * 256;
       const int cl = idx >> 5, rr = idx & 31;
-      const int col = cbase + cl;
+      const int col = col0 + cl;
       const long long row = r0 + rr;
       const bool ok = col >= 0 && col < n && row < m;
-      cp_async_elem(ring + ((g % 3) * 32 + cl) * kDColStride + rr, ok ? A + (long long)col * lda + row : A, ok);
+      cp_async_elem(dst + cl * kDColStride + rr, ok ? A + (long long)col * lda + row : A, ok);
     }
     cp_async_commit();
   };
@@ -149,41 +179,68 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
       bulk_g2s_nowait(qbuf + (w & 1) * kDQ, qpass + (size_t)w * kDQ, kDQ * 8, bar);
     }
   };
-  // prologue: groups 0 and 1 (window 0), Q_0
-  load_group(0);
-  load_group(1);
+  __syncthreads();
+  // prologue: window 0's carried half (columns -31..0) and new half (1..32), Q_0
+  load_cols(cbuf + 32 * kDColStride, -kDKB + 1);
+  load_cols(nbuf, 1);
   issue_q(0);
   const int nt = warp;  // this warp's 8 output columns of the window
+  unsigned long long mask_next = __ldg(mpass);  // nonzero 8x8 tiles of Q_w
   for (int w = 0; w < nwin; ++w) {
-    // prefetch: the next window's new columns (group w + 2) and Q_{w+1}
-    if (w + 1 < nwin) load_group(w + 2); else cp_async_commit();
+    cp_async_wait_group<0>();  // this thread's copies for window w have landed
+    __syncthreads();           // everyone's copies and window w-1's carried outputs; and
+                               // every read of window w-1's buffers is done
+    // prefetch the next window's new columns and Q_{w+1} into window w-1's buffers
+    if (w + 1 < nwin) load_cols(nbuf + ((w + 1) & 1) * 32 * kDColStride, (w + 1) * kDNB + 1);
     issue_q(w + 1);
-    cp_async_wait_group<1>();  // groups w, w + 1 have landed (this thread's copies)
-    __syncthreads();           // ... everyone's copies, and window w-1's carried outputs
     mbar_wait(&qbar[w & 1], (uint32_t)(w >> 1) & 1u);
     const double* const qs = qbuf + (w & 1) * kDQ;
-    const unsigned long long mask = __ldg(mpass + w);
-    double acc[4][2];
+    const double* const xc = cbuf + ((w + 1) & 1) * 32 * kDColStride;  // window columns 0..31
+    const double* const xn = nbuf + (w & 1) * 32 * kDColStride;        // window columns 32..63
+    const unsigned long long mask = mask_next;
+    if (w + 1 < nwin) mask_next = __ldg(mpass + w + 1);  // one window ahead: off the critical path
+    // two accumulator sets (k-tiles 0..3 and 4..7 of the window) so every warp keeps eight
+    // independent DMMA chains in flight; the k-steps of the two halves interleave
+    double acc[2][4][2];
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt) acc[rt][0] = acc[rt][1] = 0.0;
-    const int sbase = (w % 3) * 32;  // ring slot of the window's first column
+    for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-    for (int kt = 0; kt < 8; ++kt) {
-      if (!((mask >> (kt * 8 + nt)) & 1ull)) continue;
+      for (int rt = 0; rt < 4; ++rt) acc[hf][rt][0] = acc[hf][rt][1] = 0.0;
+    auto kstep = [&](int hf, int ks) {  // one k-step (4 window columns) into acc[hf]
+      const double b = qs[(ks * 8 + nt) * 32 + lane];
+      const int kc = ks * 4 + (lane & 3);  // window column of this lane's A element
+      const double* x = (hf == 0 ? xc + kc * kDColStride : xn + (kc - 32) * kDColStride) + (lane >> 2);
+      double a[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int ks = kt * 2 + h;
-        const double b = qs[(ks * 8 + nt) * 32 + lane];
-        int slot = sbase + ks * 4 + (lane & 3);
-        if (slot >= kDRing) slot -= kDRing;
-        const double* xc = ring + slot * kDColStride + (lane >> 2);
+      for (int rt = 0; rt < 4; ++rt) a[rt] = x[rt * 8];
 #pragma unroll
-        for (int rt = 0; rt < 4; ++rt) dmma884(acc[rt], xc[rt * 8], b);
+      for (int rt = 0; rt < 4; ++rt) dmma884(acc[hf][rt], a[rt], b);
+    };
+#pragma unroll
+    for (int kt = 0; kt < 4; ++kt) {
+      const bool lo = (mask >> (kt * 8 + nt)) & 1ull;
+      const bool hi = (mask >> ((kt + 4) * 8 + nt)) & 1ull;
+      if (lo && hi) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          kstep(0, kt * 2 + h);
+          kstep(1, (kt + 4) * 2 + h);
+        }
+      } else if (lo) {
+        kstep(0, kt * 2);
+        kstep(0, kt * 2 + 1);
+      } else if (hi) {
+        kstep(1, (kt + 4) * 2);
+        kstep(1, (kt + 4) * 2 + 1);
       }
     }
-    __syncthreads();  // all reads of groups w, w + 1 and of Q_w are done
-    // outputs: columns 0..31 of the window are final for this pass (to A), 32..63 are
-    // carried into the next window (group w + 1's slots, in place)
+#pragma unroll
+    for (int rt = 0; rt < 4; ++rt) {
+      acc[0][rt][0] += acc[1][rt][0];
+      acc[0][rt][1] += acc[1][rt][1];
+    }
+    // outputs: window columns 0..31 are final for this pass (to A), 32..63 are carried
+    double* const cout = cbuf + (w & 1) * 32 * kDColStride;
     const int ocol = nt * 8 + (lane & 3) * 2;  // window column of acc[.][0]
 #pragma unroll
     for (int rt = 0; rt < 4; ++rt) {
@@ -194,25 +251,24 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
         if (nt < 4) {
           const int col = w * kDNB - kDKB + 1 + wc;
           const long long row = r0 + rr;
-          if (col >= 0 && col < n && row < m) A[(long long)col * lda + row] = acc[rt][e];
+          if (col >= 0 && col < n && row < m) A[(long long)col * lda + row] = acc[0][rt][e];
         } else {
-          int slot = sbase + wc;
-          if (slot >= kDRing) slot -= kDRing;
-          ring[slot * kDColStride + rr] = acc[rt][e];
+          cout[(wc - 32) * kDColStride + rr] = acc[0][rt][e];
         }
       }
     }
   }
   cp_async_wait_group<0>();
   __syncthreads();
-  // the last window's carried columns (group nwin) are final too
+  // the last window's carried columns are final too
   {
-    const int g = nwin;
+    const double* const last = cbuf + ((nwin - 1) & 1) * 32 * kDColStride;
+    const int col0 = nwin * kDNB - kDKB + 1;
     for (int idx = tid; idx < 32 * kDRows; idx += 256) {
       const int cl = idx / kDRows, rr = idx % kDRows;
-      const int col = g * 32 - kDKB + 1 + cl;
+      const int col = col0 + cl;
       const long long row = r0 + rr;
-      if (col >= 0 && col < n && row < m) A[(long long)col * lda + row] = ring[((g % 3) * 32 + cl) * kDColStride + rr];
+      if (col >= 0 && col < n && row < m) A[(long long)col * lda + row] = last[cl * kDColStride + rr];
     }
   }
 }
@@ -233,11 +289,21 @@ int dmma_run(double* A, int64_t m, int64_t n, int64_t lda, const double* C, cons
   double* q = reinterpret_cast<double*>(workspace);
   unsigned long long* masks = reinterpret_cast<unsigned long long*>(q + (size_t)passes * nwin * kDQ);
   dim3 qg((unsigned)nwin, (unsigned)passes);
+  const size_t qsmem = sizeof(double2) * kDKB * kDPairs;
+  static std::atomic<int> qconfigured{0};
+  if (!qconfigured.load()) {
+    if (cudaFuncSetAttribute(rs_dmma_q_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(rs_dmma_q_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem) !=
+            cudaSuccess)
+      return -1;
+    qconfigured.store(1);
+  }
   if (refl)
-    rs_dmma_q_kernel<true><<<qg, kDW, 0, st>>>(q, masks, C, S, ldcs, (int)n, (int)k, rev);
+    rs_dmma_q_kernel<true><<<qg, kDW, qsmem, st>>>(q, masks, C, S, ldcs, (int)n, (int)k, rev);
   else
-    rs_dmma_q_kernel<false><<<qg, kDW, 0, st>>>(q, masks, C, S, ldcs, (int)n, (int)k, rev);
-  const size_t smem = (size_t)2 * kDQ * 8 + (size_t)kDRing * kDColStride * 8 + 2 * sizeof(uint64_t);
+    rs_dmma_q_kernel<false><<<qg, kDW, qsmem, st>>>(q, masks, C, S, ldcs, (int)n, (int)k, rev);
+  const size_t smem = (size_t)2 * kDQ * 8 + (size_t)4 * 32 * kDColStride * 8 + 2 * sizeof(uint64_t);
   static std::atomic<int> configured{0};
   if (!configured.load()) {
     if (cudaFuncSetAttribute(rs_dmma_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
