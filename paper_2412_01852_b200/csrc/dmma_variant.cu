@@ -140,7 +140,10 @@ __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
 // cp.async one window ahead). Outputs 0..31 are final for the pass and go to A, outputs
 // 32..63 go to cbuf[w&1] for window w+1: one __syncthreads per window orders everything
 // (buffers alternate, so no window writes what the previous one may still read).
-__global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restrict__ A, long long m, long long lda,
+// NW = 8 warps (each 4 row tiles of one column tile; two CTAs fit an SM) or 16 (2 row
+// tiles each; one CTA per SM, for grids too small to give every SM two CTAs).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) rs_dmma_apply_kernel(double* __restrict__ A, long long m, long long lda,
                                                                int n, const double* __restrict__ qpass,
                                                                const unsigned long long* __restrict__ mpass,
                                                                int nwin) {
@@ -149,6 +152,8 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
   double* const cbuf = qbuf + 2 * kDQ;                  // 2 x 32 columns x kDColStride (carried)
   double* const nbuf = cbuf + 2 * 32 * kDColStride;     // 2 x 32 columns x kDColStride (new)
   uint64_t* const qbar = reinterpret_cast<uint64_t*>(nbuf + 2 * 32 * kDColStride);
+  constexpr int NT = NW * 32;
+  constexpr int RT = 32 / NW;  // 8-row tiles per warp
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long r0 = (long long)blockIdx.x * kDRows;
   if (tid == 0) {
@@ -160,8 +165,8 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
   // columns or rows outside the matrix are zero-filled)
   auto load_cols = [&](double* dst, int col0) {
 #pragma unroll
-    for (int it = 0; it < 4; ++it) {
-      const int idx = tid + it * 256;
+    for (int it = 0; it < 32 * kDRows / NT; ++it) {
+      const int idx = tid + it * NT;
       const int cl = idx >> 5, rr = idx & 31;
       const int col = col0 + cl;
       const long long row = r0 + rr;
@@ -184,7 +189,8 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
   load_cols(cbuf + 32 * kDColStride, -kDKB + 1);
   load_cols(nbuf, 1);
   issue_q(0);
-  const int nt = warp;  // this warp's 8 output columns of the window
+  const int nt = warp & 7;         // this warp's 8 output columns of the window
+  const int rt0 = (warp >> 3) * RT;  // and its first 8-row tile
   unsigned long long mask_next = __ldg(mpass);  // nonzero 8x8 tiles of Q_w
   for (int w = 0; w < nwin; ++w) {
     cp_async_wait_group<0>();  // this thread's copies for window w have landed
@@ -201,20 +207,21 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
     if (w + 1 < nwin) mask_next = __ldg(mpass + w + 1);  // one window ahead: off the critical path
     // two accumulator sets (k-tiles 0..3 and 4..7 of the window) so every warp keeps eight
     // independent DMMA chains in flight; the k-steps of the two halves interleave
-    double acc[2][4][2];
+    double acc[2][RT][2];
 #pragma unroll
     for (int hf = 0; hf < 2; ++hf)
 #pragma unroll
-      for (int rt = 0; rt < 4; ++rt) acc[hf][rt][0] = acc[hf][rt][1] = 0.0;
+      for (int rt = 0; rt < RT; ++rt) acc[hf][rt][0] = acc[hf][rt][1] = 0.0;
     auto kstep = [&](int hf, int ks) {  // one k-step (4 window columns) into acc[hf]
       const double b = qs[(ks * 8 + nt) * 32 + lane];
       const int kc = ks * 4 + (lane & 3);  // window column of this lane's A element
-      const double* x = (hf == 0 ? xc + kc * kDColStride : xn + (kc - 32) * kDColStride) + (lane >> 2);
-      double a[4];
+      const double* x =
+          (hf == 0 ? xc + kc * kDColStride : xn + (kc - 32) * kDColStride) + rt0 * 8 + (lane >> 2);
+      double a[RT];
 #pragma unroll
-      for (int rt = 0; rt < 4; ++rt) a[rt] = x[rt * 8];
+      for (int rt = 0; rt < RT; ++rt) a[rt] = x[rt * 8];
 #pragma unroll
-      for (int rt = 0; rt < 4; ++rt) dmma884(acc[hf][rt], a[rt], b);
+      for (int rt = 0; rt < RT; ++rt) dmma884(acc[hf][rt], a[rt], b);
     };
 #pragma unroll
     for (int kt = 0; kt < 4; ++kt) {
@@ -235,7 +242,7 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
       }
     }
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt) {
+    for (int rt = 0; rt < RT; ++rt) {
       acc[0][rt][0] += acc[1][rt][0];
       acc[0][rt][1] += acc[1][rt][1];
     }
@@ -243,8 +250,8 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
     double* const cout = cbuf + (w & 1) * 32 * kDColStride;
     const int ocol = nt * 8 + (lane & 3) * 2;  // window column of acc[.][0]
 #pragma unroll
-    for (int rt = 0; rt < 4; ++rt) {
-      const int rr = rt * 8 + (lane >> 2);
+    for (int rt = 0; rt < RT; ++rt) {
+      const int rr = (rt0 + rt) * 8 + (lane >> 2);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int wc = ocol + e;
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(256, 1) rs_dmma_apply_kernel(double* __restric
   {
     const double* const last = cbuf + ((nwin - 1) & 1) * 32 * kDColStride;
     const int col0 = nwin * kDNB - kDKB + 1;
-    for (int idx = tid; idx < 32 * kDRows; idx += 256) {
+    for (int idx = tid; idx < 32 * kDRows; idx += NT) {
       const int cl = idx / kDRows, rr = idx % kDRows;
       const int col = col0 + cl;
       const long long row = r0 + rr;
@@ -306,18 +313,31 @@ int dmma_run(double* A, int64_t m, int64_t n, int64_t lda, const double* C, cons
   const size_t smem = (size_t)2 * kDQ * 8 + (size_t)4 * 32 * kDColStride * 8 + 2 * sizeof(uint64_t);
   static std::atomic<int> configured{0};
   if (!configured.load()) {
-    if (cudaFuncSetAttribute(rs_dmma_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(rs_dmma_apply_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(rs_dmma_apply_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
       return -1;
     configured.store(1);
   }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   // reverse order: mirror the columns (base at the last column, negative stride)
   double* Ab = rev ? A + (long long)(n - 1) * lda : A;
   const long long ld = rev ? -lda : lda;
   const unsigned grid = (unsigned)((m + kDRows - 1) / kDRows);
-  for (int p = 0; p < passes; ++p)
-    rs_dmma_apply_kernel<<<grid, 256, smem, st>>>(Ab, m, ld, (int)n, q + (size_t)p * nwin * kDQ,
-                                                  masks + (size_t)p * nwin, nwin);
+  // measured (B200): 8-warp CTAs when the grid gives every SM two of them (65536 x 2048:
+  // 22.4 vs 18.4 TF/s), 16-warp CTAs otherwise (4096^2: 15.0 vs 14.1 TF/s)
+  const bool wide = grid < 2u * (unsigned)sms;
+  for (int p = 0; p < passes; ++p) {
+    if (wide)
+      rs_dmma_apply_kernel<16><<<grid, 512, smem, st>>>(Ab, m, ld, (int)n, q + (size_t)p * nwin * kDQ,
+                                                        masks + (size_t)p * nwin, nwin);
+    else
+      rs_dmma_apply_kernel<8><<<grid, 256, smem, st>>>(Ab, m, ld, (int)n, q + (size_t)p * nwin * kDQ,
+                                                       masks + (size_t)p * nwin, nwin);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? passes + 1 : -1;
 }
 
