@@ -11,9 +11,9 @@
 
 namespace rsk {
 
-template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT, int K>
+template <typename T, bool STRICT, bool REFL, bool HS, bool LEFT, int K, int MW>
 cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) {
-  auto kern = rs_pipeline_kernel<T, K, rows_for(sizeof(T)), STRICT, REFL, HS, LEFT>;
+  auto kern = rs_pipeline_kernel<T, K, rows_for(sizeof(T)), STRICT, REFL, HS, LEFT, MW>;
   static std::atomic<int> configured{0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -28,21 +28,26 @@ cudaError_t launch_pipeline(const cudaLaunchConfig_t& cfg, const PipeParams& P) 
   return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
-#define RS_INST(HS, LEFT, K)                                                                                  \
-  template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, HS, LEFT, K>( \
+#define RS_INST(HS, LEFT, K, MW)                                                                              \
+  template cudaError_t launch_pipeline<RS_VARIANT_T, RS_VARIANT_STRICT != 0, RS_VARIANT_REFL != 0, HS, LEFT, K, MW>( \
       const cudaLaunchConfig_t&, const PipeParams&);
-RS_INST(false, false, 8)
-RS_INST(true, false, 8)
-RS_INST(false, true, 8)
-RS_INST(true, true, 8)
-// the wide windows (right side): 16 sweeps for fp32, 12 for fp64
+RS_INST(false, false, 8, max_warps_for(sizeof(RS_VARIANT_T), false, 8))
+RS_INST(true, false, 8, max_warps_for(sizeof(RS_VARIANT_T), false, 8))
+RS_INST(false, true, 8, max_warps_for(sizeof(RS_VARIANT_T), true, 8))
+RS_INST(true, true, 8, max_warps_for(sizeof(RS_VARIANT_T), true, 8))
+// fp64 right side: the 168-register build for plans of <= 12 warps per CTA
+#if !RS_VARIANT_F32
+RS_INST(false, false, 8, kSmallCtaWarps)
+RS_INST(true, false, 8, kSmallCtaWarps)
+#endif
+// the wide windows (right side, off by default): 16 sweeps for fp32, 12 for fp64
 #if RS_VARIANT_F32 && RS_F32_WIDE
-RS_INST(false, false, 16)
-RS_INST(true, false, 16)
+RS_INST(false, false, 16, max_warps_for(4, false, 16))
+RS_INST(true, false, 16, max_warps_for(4, false, 16))
 #endif
 #if !RS_VARIANT_F32 && RS_F64_WIDE
-RS_INST(false, false, 12)
-RS_INST(true, false, 12)
+RS_INST(false, false, 12, max_warps_for(8, false, 12))
+RS_INST(true, false, 12, max_warps_for(8, false, 12))
 #endif
 
 }  // namespace rsk

@@ -425,21 +425,31 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool left = g.os != 1;  // owners are columns: owner-major rings, coalesced A I/O
+  constexpr size_t TS = sizeof(T);
+  constexpr int MWR = max_warps_for(TS, false, kK), MWL = max_warps_for(TS, true, kK);
+  // fp64 right side: plans of <= 12 warps per CTA run the 168-register build
+  const bool small = TS == 8 && !left && lp.nw <= kSmallCtaWarps && !getenv("RS_NO_SMALL_CTA");
   if (g.kw != kK) {
-    constexpr int KW = wide_k(sizeof(T));
-    if constexpr ((sizeof(T) == 4 && RS_F32_WIDE) || (sizeof(T) == 8 && RS_F64_WIDE)) {
+    constexpr int KW = wide_k(TS);
+    if constexpr ((TS == 4 && RS_F32_WIDE) || (TS == 8 && RS_F64_WIDE)) {
+      constexpr int MWW = max_warps_for(TS, false, KW);
       if (left || g.kw != KW) return fail(RS_EUNSUPPORTED, "wide window: right-side launches only");
-      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, KW>(cfg, P)
-             : launch_pipeline<T, STRICT, REFL, false, false, KW>(cfg, P);
+      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, KW, MWW>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false, KW, MWW>(cfg, P);
     } else {
       return fail(RS_EUNSUPPORTED, "wide window not built");
     }
-  } else if (hs) {
-    e = left ? launch_pipeline<T, STRICT, REFL, true, true, kK>(cfg, P)
-             : launch_pipeline<T, STRICT, REFL, true, false, kK>(cfg, P);
+  } else if (left) {
+    e = hs ? launch_pipeline<T, STRICT, REFL, true, true, kK, MWL>(cfg, P)
+           : launch_pipeline<T, STRICT, REFL, false, true, kK, MWL>(cfg, P);
+  } else if (small) {
+    if constexpr (TS == 8) {
+      e = hs ? launch_pipeline<T, STRICT, REFL, true, false, kK, kSmallCtaWarps>(cfg, P)
+             : launch_pipeline<T, STRICT, REFL, false, false, kK, kSmallCtaWarps>(cfg, P);
+    }
   } else {
-    e = left ? launch_pipeline<T, STRICT, REFL, false, true, kK>(cfg, P)
-             : launch_pipeline<T, STRICT, REFL, false, false, kK>(cfg, P);
+    e = hs ? launch_pipeline<T, STRICT, REFL, true, false, kK, MWR>(cfg, P)
+           : launch_pipeline<T, STRICT, REFL, false, false, kK, MWR>(cfg, P);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pipeline launch: ") + cudaGetErrorString(e));
