@@ -182,6 +182,16 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
                        int* grid_ctas, int* warps_per_cta, int64_t* units, int* band_width,
                        int* rows_per_tile, size_t* smem_bytes);
 
+/* The compile-time tile shape of the pipeline kernel for (dtype, side): sweeps per unit
+ * window (the reference's k_r), rows per thread (tile rows = 32 * rows_per_thread, the
+ * reference's m_r), ring depth in chunks, and the warps-per-CTA bounds of the two register
+ * budgets the kernel is built for (a build for at most `small_cta_warps` warps, 0 if the
+ * family has none, and one for up to `max_warps`). Needs no GPU; the host-side tile model
+ * (paper_2412_01852_b200/model.py, the counterpart of the reference's choose_block_sizes,
+ * blocking.py:115-147) must choose exactly these values. Any out-pointer may be NULL. */
+rs_status rs_tile_shape(int dtype, int side, int* window_sweeps, int* rows_per_thread, int* ring_chunks,
+                        int* small_cta_warps, int* max_warps);
+
 /* Measured FMA-pipe peak of the current device (TFLOP/s, 2 flops per FMA) for dtype
  * RS_DTYPE_F64 (DFMA) or RS_DTYPE_F32 (FFMA): the roofline denominator for this
  * FP-bound path. Synchronous (~10 ms). Not on the apply path. */

@@ -39,6 +39,7 @@ EXPORTS = (
     "rs_apply_algo_f64",
     "rs_apply_algo_f32",
     "rs_plan_info",
+    "rs_tile_shape",
     "rs_pack_f64",
     "rs_pack_f32",
     "rs_pack_fast_f64",
@@ -124,6 +125,8 @@ def _declare(lib):
     lib.rs_plan_info.argtypes = [i64, i64, i64, i32, i32, i32,
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i64),
                                  ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(sz)]
+    lib.rs_tile_shape.restype = i32
+    lib.rs_tile_shape.argtypes = [i32, i32] + [ctypes.POINTER(i32)] * 5
     lib.rs_launch_count.restype = i64
     lib.rs_launch_count.argtypes = []
     lib.rs_fma_peak_tflops.restype = i32
@@ -178,6 +181,15 @@ def plan_info(m: int, n: int, k: int, side: int = SIDE_RIGHT, kind: int = KIND_R
     check(st, "rs_plan_info")
     return dict(grid_ctas=grid.value, warps_per_cta=nw.value, units=units.value,
                 band_width=bw.value, rows_per_tile=rpt.value, smem_bytes=smem.value)
+
+
+def tile_shape(dtype: int = DTYPE_F64, side: int = SIDE_RIGHT) -> dict:
+    """Compile-time tile shape of the pipeline kernel (no GPU needed): what
+    model.choose_tile_shape must reproduce."""
+    v = [ctypes.c_int() for _ in range(5)]
+    check(load().rs_tile_shape(dtype, side, *[ctypes.byref(x) for x in v]), "rs_tile_shape")
+    return dict(window_sweeps=v[0].value, rows_per_thread=v[1].value, ring_chunks=v[2].value,
+                small_cta_warps=v[3].value, max_warps=v[4].value)
 
 
 def fma_peak_tflops(dtype: int = DTYPE_F64, stream=None) -> float:

@@ -81,6 +81,7 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
         return out
     extra = list(extra or []) + os.environ.get("RS_NVCC_EXTRA", "").split()
     nvcc = nvcc_path()
+    only = [u for u in os.environ.get("RS_BUILD_ONLY", "").split(",") if u] if out != OUT else []
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     os.makedirs(OBJ_CACHE, exist_ok=True)
     units = [("host", [], SRC, [SRC, DEVICE_HDR, HDR]), ("dmma", [], DMMA_SRC, [DMMA_SRC, DEVICE_HDR, HDR])]
@@ -92,6 +93,11 @@ def build_library(force: bool = False, verbose: bool = False, out: str | None = 
     for name, defs, src, srcdeps in units:
         base = [nvcc, *NVCC_FLAGS, *extra, *inc, *defs]
         obj = os.path.join(OBJ_CACHE, f"{name}-{_key(base + [src], srcdeps)}.o")
+        if only and name not in only:
+            # developer experiments (RS_BUILD_ONLY=host,pipe_double_0_0): every other unit
+            # is compiled (or taken from the cache) without the extra flags
+            base = [nvcc, *NVCC_FLAGS, *inc, *defs]
+            obj = os.path.join(OBJ_CACHE, f"{name}-{_key(base + [src], srcdeps)}.o")
         jobs.append((obj, base + ["-c", "-o", obj + ".tmp", src]))
     todo = [j for j in jobs if not os.path.exists(j[0])]
 

@@ -1053,6 +1053,21 @@ rs_status rs_plan_info(int64_t m, int64_t n, int64_t k, int side, int kind, int 
   return RS_OK;
 }
 
+rs_status rs_tile_shape(int dtype, int side, int* window_sweeps, int* rows_per_thread, int* ring_chunks,
+                        int* small_cta_warps, int* max_warps) {
+  g_err.clear();
+  if (dtype != RS_DTYPE_F64 && dtype != RS_DTYPE_F32) return fail(RS_EINVAL, "bad dtype");
+  if (side != RS_SIDE_LEFT && side != RS_SIDE_RIGHT) return fail(RS_EINVAL, "bad side");
+  const size_t tsz = dtype == RS_DTYPE_F64 ? 8 : 4;
+  const bool left = side == RS_SIDE_LEFT;
+  if (window_sweeps) *window_sweeps = kK;
+  if (rows_per_thread) *rows_per_thread = rows_for(tsz);
+  if (ring_chunks) *ring_chunks = stages_for(tsz);
+  if (small_cta_warps) *small_cta_warps = (tsz == 8 && !left) ? kSmallCtaWarps : 0;
+  if (max_warps) *max_warps = max_warps_for(tsz, left, kK);
+  return RS_OK;
+}
+
 int64_t rs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 rs_status rs_pack_f64(const double* C, const double* S, int64_t ldcs, int64_t m, int64_t n, int64_t k, int side,

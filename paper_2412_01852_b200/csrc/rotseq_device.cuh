@@ -568,13 +568,24 @@ __device__ __forceinline__ void dispatch_width(int Kb, F&& f) {
 // OUTS: the output columns go to shared memory (the next unit's ring, or the left side's
 // staging slot) at obase + u*OSU + r*OSR elements and are stored with STS; otherwise to A
 // through the generic pointers op[r] (stride ostr[r]).
-template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT, bool OUTS>
+// FIRST (with EDGE): block 0 of a unit whose first chunk lies inside the matrix (the caller
+// guarantees len >= K+1): nothing to emit, every column of the chunk valid, and rotation
+// (u, l) in range iff l < u — a compile-time triangle, so half of the block's rotations
+// vanish and the rest carry one width test instead of the generic edge tests.
+// final_exit (EDGE, the draining last block): the unit's work ends with the store of column
+// len-1; when `early_out` is set (ring output) the consumer's "full" barrier is signalled
+// right there, and the rest of the block (rotations that are all out of range) is skipped.
+// Both shorten the hand-off lag per chain hop.
+template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT, bool OUTS,
+          bool FIRST = false>
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* islot, T* const (&op)[R], const long long (&ostr)[R],
                                           T* obase, int b, int len, int Kb, int lane, bool has_in_rt,
                                           bool has_out_rt, uint64_t* sub_in = nullptr, uint32_t sub_par = 0,
-                                          uint64_t* sub_out = nullptr) {
+                                          uint64_t* sub_out = nullptr, bool final_exit = false,
+                                          uint64_t* early_out = nullptr) {
+  static_assert(!FIRST || EDGE, "FIRST is a variant of the edge block");
   // sub-chunk hand-off (kSub > 1, right side): wait for sub-chunk h before loading its first
   // column; announce sub-chunk h once its last column is stored
   constexpr int SUBW = (K + 1) / kSub;
@@ -584,8 +595,8 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   constexpr int TR = 32 * R;
   constexpr int NL = EDGE ? K : KB;
   const long long c0 = (long long)b * (K + 1);
-  const bool has_in = !EDGE || has_in_rt;
-  const bool has_out = !EDGE || has_out_rt;
+  const bool has_in = !EDGE || FIRST || has_in_rt;
+  const bool has_out = !FIRST && (!EDGE || has_out_rt);
   // scaled mode: the emitted column is multiplied back by its scale (after the block's records)
   constexpr bool PAIR = kPairRecs<T, REFL>;
   const int NR = recs_per_wave(EDGE ? Kb : KB, PAIR);  // records per wave
@@ -595,7 +606,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   for (int r = 0; r < R; ++r) q[r] = op[r];
   auto load_col = [&](int u, T (&dst)[R]) {
     const long long col = c0 + u;
-    if (!EDGE || (has_in && col < len)) {
+    if (!EDGE || FIRST || (has_in && col < len)) {
 #pragma unroll
       for (int r = 0; r < R; ++r) dst[r] = islot[LEFT ? (lane + 32 * r) * (K + 1) + u : u * TR + lane + 32 * r];
     } else {
@@ -649,6 +660,15 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
           if (lane == 0) mbar_arrive(&sub_out[u / SUBW]);
         }
       }
+      if constexpr (EDGE && !FIRST) {
+        if (final_exit && col == (long long)len - 1) {  // the unit's last column is out
+          if (early_out != nullptr) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(early_out);
+          }
+          return;
+        }
+      }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) w[r][u] = nv[r];
@@ -657,7 +677,10 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
       constexpr int M = K + 1;
       const int sx = (u - 1 - l + 2 * M) % M;
       const int sy = (sx + 1) % M;
-      if (EDGE) {
+      if constexpr (FIRST) {
+        if (l >= u) continue;  // j = u - 1 - l < 0 (compile time)
+        if (l >= Kb) continue;
+      } else if (EDGE) {
         const long long j = c0 + u - 1 - l;
         if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
       }
@@ -1299,9 +1322,10 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     int done_sig = 0;  // host streaming: chunks already released by this (final) unit
     // One block: protocol + compute. KB / EDGE are compile-time so the interior loop
     // carries no per-block branches beyond this unit's hand-off protocol.
-    auto block = [&](int b, auto kb_c, auto edge_c) {
+    auto block = [&](int b, auto kb_c, auto edge_c, auto first_c) {
       constexpr int KB = decltype(kb_c)::value;
       constexpr bool EDGE = decltype(edge_c)::value;
+      constexpr bool FIRST = decltype(first_c)::value;
       unsigned long long t0 = trace_clock();
       const bool pair_start = (b & 1) == 0;
       if (pair_start && b + 2 < nblk) issue_coef(b + 2, (cseq + 1) & 1);
@@ -1361,13 +1385,15 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 #else
           T* const obase_s = op[0];
 #endif
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true>(w, cbp, islot, op, ostr, obase_s, b, len, Kb,
-                                                                          lane, b < nchunk, b >= 1, sub_in, sub_par,
-                                                                          sub_out);
+          // the draining last block signals the consumer at its final column and stops there
+          uint64_t* const early = (SUB == 1 && b == nblk - 1) ? &full_out[oseq % S] : nullptr;
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true, FIRST>(
+              w, cbp, islot, op, ostr, obase_s, b, len, Kb, lane, b < nchunk, b >= 1, sub_in, sub_par, sub_out,
+              b == nblk - 1, early);
         } else {
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false>(w, cbp, islot, op, ostr, nullptr, b, len,
-                                                                           Kb, lane, b < nchunk, b >= 1, sub_in,
-                                                                           sub_par, sub_out);
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false, FIRST>(
+              w, cbp, islot, op, ostr, nullptr, b, len, Kb, lane, b < nchunk, b >= 1, sub_in, sub_par, sub_out,
+              b == nblk - 1, nullptr);
         }
       }
       __syncwarp();
@@ -1406,7 +1432,8 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
         } else if (has_in) {
           st_release_shared(consumed_in, iseq + 1u);
         }
-        if (SUB == 1 && outring && has_out) mbar_arrive(&full_out[oseq % S]);
+        // (the last block signalled from inside run_block, at its final column)
+        if (SUB == 1 && outring && has_out && !(P.ring_sts && b == nblk - 1)) mbar_arrive(&full_out[oseq % S]);
         if (dst == DST_FLAG && has_out &&
             (b < 2 * kFlagEvery || (b & (kFlagEvery - 1)) == 0 || b >= nblk - RS_FLAG_TAIL)) {
           // the warp barrier above orders every lane's stores before lane 0's gpu-scope
@@ -1448,12 +1475,16 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     using I8 = std::integral_constant<int, K>;
     const int full_hi = (len - 1 - K >= 0) ? (len - 1 - K) / (K + 1) : 0;
     const int interior_end = full_hi + 1;  // blocks [1, full_hi] are interior
-    block(0, I8{}, T_{});
+    // block 0: the compile-time triangle when chunk 0 and block 1 lie inside the matrix
+    if (interior_end > 1)
+      block(0, I8{}, T_{}, T_{});
+    else
+      block(0, I8{}, T_{}, F_{});
     // interior blocks with the unit width as a compile-time constant (one loop body per width)
     dispatch_width<K, kb_min(K)>(Kb, [&](auto kb_c) {
-      for (int b = 1; b < interior_end; ++b) block(b, kb_c, F_{});
+      for (int b = 1; b < interior_end; ++b) block(b, kb_c, F_{}, F_{});
     });
-    for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{});
+    for (int b = max(1, interior_end); b < nblk; ++b) block(b, I8{}, T_{}, F_{});
     trace_unit(P.trace, warp, jr, tile, p0, Kb, src, dst, tacc);
     };
     if constexpr (SCALED_ANY) {
