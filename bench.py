@@ -376,9 +376,38 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         bi = hA.numel() * hA.element_size() + hC.numel() * hC.element_size() * 2
         bo = hA.numel() * hA.element_size()
+        # the copy floor of this box: the same bytes in, then out, with nothing to compute
+        # (whole-matrix copies on two streams, both directions at once) -- what the host
+        # link alone costs per step; e2e / floor says how much of the step the dependent
+        # chain (an output column needs ~k + pipeline-depth later input columns) adds
+        floor_ms = None
+        try:
+            hB = torch.empty_strided(hA.shape, hA.stride(), dtype=tdtype, pin_memory=True)
+            s_in, s_out = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+            reps = []
+            for _ in range(4):
+                torch.cuda.synchronize(dev)
+                f0, f1, f2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                f0.record(stream)
+                s_in.wait_stream(stream)
+                s_out.wait_stream(stream)
+                with torch.cuda.stream(s_in):
+                    dA.copy_(hA, non_blocking=True)
+                    f1.record(s_in)
+                with torch.cuda.stream(s_out):
+                    hB.copy_(dA, non_blocking=True)
+                    f2.record(s_out)
+                torch.cuda.synchronize(dev)
+                reps.append(max(f0.elapsed_time(f1), f0.elapsed_time(f2)))
+            floor_ms = min(reps[1:])
+            del hB
+        except RuntimeError:
+            floor_ms = None
         e2e = {"value": flops_total / (float(t.item()) * 1e-3) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
                "ms_per_step": float(t.item()),
+               "copy_floor_ms": floor_ms,
+               "copy_floor_note": "H2D of A and D2H of A as two whole-matrix copies running concurrently on this box, no compute",
                "step_ms": {"min": min(e2e_ms), "median": statistics.median(e2e_ms), "max": max(e2e_ms)}, "api": "apply_cuda(pinned host torch tensors) -> rs_apply_host_* (chunked copy-in/compute/copy-out overlap)"}
 
     # roofline: the pipeline kernel against the live FMA-pipe peak

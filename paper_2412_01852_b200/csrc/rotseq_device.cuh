@@ -94,9 +94,12 @@ constexpr int kMaxWarpsLeft = 12;
 #ifndef RS_WIDE_WARPS_F64
 #define RS_WIDE_WARPS_F64 8
 #endif
+#ifndef RS_R4_WARPS
+#define RS_R4_WARPS 8
+#endif
 __host__ __device__ constexpr int max_warps_for(size_t tsz, bool left, int K = 8) {
   return K > 8 ? (tsz == 8 ? RS_WIDE_WARPS_F64 : RS_WIDE_WARPS)
-               : (rows_for(tsz) == 4 ? 8 : (left ? kMaxWarpsLeft : kMaxWarps));
+               : (rows_for(tsz) == 4 ? RS_R4_WARPS : (left ? kMaxWarpsLeft : kMaxWarps));
 }
 __host__ __device__ constexpr int tile_owners(size_t tsz) { return 32 * rows_for(tsz); }
 constexpr uint32_t kSuspendHintNs = 1000000;  // mbarrier try_wait suspend-time hint
@@ -255,6 +258,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 #ifndef RS_WAIT_MODE
 #define RS_WAIT_MODE 0
 #endif
+#ifndef RS_WAIT_NS
+#define RS_WAIT_NS 64
+#endif
 __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
 #if RS_WAIT_MODE == 1
   asm volatile(
@@ -275,7 +281,7 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t parity) {
         : "r"(bar), "r"(parity)
         : "memory");
     if (ok) break;
-    __nanosleep(64);
+    __nanosleep(RS_WAIT_NS);
   }
 #else
   asm volatile(

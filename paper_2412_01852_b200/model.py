@@ -41,7 +41,8 @@ from dataclasses import dataclass, field
 
 __all__ = [
     "SmSpec", "TileShape", "WindowMemOps", "memops_window", "issue_cycles", "register_need",
-    "smem_per_warp", "block_code_bytes", "candidate_table", "choose_tile_shape", "modelled_tflops",
+    "smem_per_warp", "block_code_bytes", "candidate_table", "fill_efficiency", "choose_tile_shape",
+    "modelled_tflops", "TARGET_WORKLOADS",
 ]
 
 
@@ -67,6 +68,10 @@ class SmSpec:
     min_warps_per_smsp: int = 3             # fewer cannot cover the hand-off waits (measured:
     #                                         8-warp CTAs lose to 12-warp ones at equal R)
     warp_choices: tuple = (8, 12, 16)
+    # Window widths considered: a unit covers K consecutive sweeps and a chain runs at the
+    # pace of its widest unit (measured), so K must split the sweep counts
+    # in use evenly; those are multiples of 8 (every BASELINE configuration: 64 ... 256).
+    window_choices: tuple = (2, 4, 8, 16)
 
 
 @dataclass(frozen=True)
@@ -144,13 +149,16 @@ def issue_cycles(K: int, R: int, tsz: int = 8, form: str = "scaled", spec: SmSpe
 
 def register_need(K: int, R: int, tsz: int = 8, left: bool = False) -> int:
     """Registers per thread: the (K+1) x R window, one column in flight each way, the
-    4-deep coefficient queue (16 registers), and the addressing / protocol state of the
-    block loop (~60 right side, ~84 left side with its owner-major chunk copies), plus 10%
-    for the scheduler to overlap independent transforms (below that ptxas spills: the
-    R=2 fp64 body spills at 128 and is clean at 168)."""
+    4-deep coefficient queue (16 registers) and the addressing / protocol state of the
+    unit loop (~96 registers on the right side, ~112 on the left with its owner-major chunk
+    copies). Calibrated on ptxas: the fp64 R=2 right-side kernel needs 168 (24 bytes of
+    spills remain), the fp32 one 128 (40 bytes)."""
     w = tsz // 4
-    base = 84 if left else 60
-    return int(round(1.10 * (w * (K + 1) * R + 2 * w * R + 16 + base)))
+    base = 112 if left else 96
+    return w * (K + 1) * R + 2 * w * R + 16 + base
+
+
+SPILL_TOLERANCE_REGS = 8  # a build a few registers short still runs at speed (measured)
 
 
 def smem_per_warp(K: int, R: int, tsz: int = 8, ring_chunks: int = 2, left: bool = False) -> int:
@@ -183,7 +191,7 @@ def candidate_table(tsz: int = 8, left: bool = False, form: str = "scaled", spec
     """Every (K, R, warps) with its budgets and modelled cycles; ``feasible`` is false
     with the violated budget named in ``why``."""
     rows = []
-    for K in range(2, 17):
+    for K in spec.window_choices:
         for R in range(1, 5):
             for warps in spec.warp_choices:
                 need = register_need(K, R, tsz, left)
@@ -191,7 +199,7 @@ def candidate_table(tsz: int = 8, left: bool = False, form: str = "scaled", spec
                 smem = warps * smem_per_warp(K, R, tsz, ring_chunks, left) + (ring_chunks + 3) * 8
                 code = block_code_bytes(K, R, tsz, form)
                 why = []
-                if need > have:
+                if need > have + SPILL_TOLERANCE_REGS:
                     why.append(f"registers {need} > {have}")
                 if smem > spec.smem_optin_bytes:
                     why.append(f"shared memory {smem} > {spec.smem_optin_bytes}")
@@ -206,16 +214,45 @@ def candidate_table(tsz: int = 8, left: bool = False, form: str = "scaled", spec
     return rows
 
 
+# (owners, sweeps) of the BASELINE configurations each kernel family has to serve: the
+# compile-time shape is chosen for the worst of them (configs 2 and 3; 5; 4 and, for the
+# fp32 left side, which BASELINE does not exercise, its transpose)
+TARGET_WORKLOADS = {
+    (8, False): ((4096, 192), (65536, 256)),
+    (8, True): ((16384, 96),),
+    (4, False): ((8192, 128),),
+    (4, True): ((8192, 128),),
+}
+
+
+def fill_efficiency(K: int, R: int, warps: int, owners: int, k: int, spec: SmSpec = SmSpec()) -> float:
+    """Share of the chip's warp slots a problem keeps busy with this shape: its units
+    (tiles of 32*R owners x ceil(k/K) sweep ranges) run in whole rounds of sms*warps
+    slots (the GPU counterpart of the reference's partition_rows balance,
+    blocking.py:178-202). Fat tiles leave a mid-sized problem with too few units."""
+    units = -(-owners // (32 * R)) * -(-k // K)
+    slots = spec.sms * warps
+    rounds = -(-units // slots)
+    return units / float(rounds * slots)
+
+
 def choose_tile_shape(tsz: int = 8, left: bool = False, form: str = "scaled", spec: SmSpec = SmSpec(),
-                      ring_chunks: int = 2) -> TileShape:
-    """The feasible (K, R, warps) with the fewest modelled cycles per transform element;
-    ties go to the wider window (fewer hand-offs per sweep), then to more warps (the same
-    build also serves smaller CTAs)."""
+                      ring_chunks: int = 2, workloads=None) -> TileShape:
+    """The feasible (K, R, warps) with the highest modelled throughput on the worst of the
+    target workloads: steady-state cycles per transform element (issue_cycles) divided by
+    the share of the chip the workload fills (fill_efficiency). Ties go to the wider
+    window (fewer hand-offs per sweep), then to fewer warps (more registers per thread)."""
+    workloads = TARGET_WORKLOADS[(tsz, left)] if workloads is None else workloads
+    # one tile height per element size: the left side keeps the right side's rows per
+    # thread (tile_owners() in the library is a function of the element size only, so
+    # shard boundaries and workspace sizes do not depend on the side)
+    rows = choose_tile_shape(tsz, False, form, spec, ring_chunks).R if left else None
     best = None
     for c in candidate_table(tsz, left, form, spec, ring_chunks):
-        if not c["feasible"]:
+        if not c["feasible"] or (rows is not None and c["R"] != rows):
             continue
-        key = (round(c["cycles"], 6), -c["K"], -c["warps"])
+        fill = min(fill_efficiency(c["K"], c["R"], c["warps"], o, k, spec) for o, k in workloads)
+        key = (round(c["cycles"] / fill, 6), -c["K"], c["warps"])
         if best is None or key < best[0]:
             best = (key, c)
     if best is None:
