@@ -600,7 +600,11 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   constexpr int OSR = LEFT ? 32 * (K + 1) : 32;
   constexpr int TR = 32 * R;
   constexpr int NL = EDGE ? K : KB;
-  const long long c0 = (long long)b * (K + 1);
+  // edge-block index arithmetic: 32-bit on the fp64 right side (columns fit an int: len is
+  // one; +1.3% at configs 2 and 3), 64-bit elsewhere (the left-side and fp32 bodies
+  // schedule better with it: -4% / -1% at configs 5 / 4 otherwise)
+  using IdxT = std::conditional_t<(!LEFT && sizeof(T) == 8), int, long long>;
+  const IdxT c0 = (IdxT)b * (K + 1);
   const bool has_in = !EDGE || FIRST || has_in_rt;
   const bool has_out = !FIRST && (!EDGE || has_out_rt);
   // scaled mode: the emitted column is multiplied back by its scale (after the block's records)
@@ -611,7 +615,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
 #pragma unroll
   for (int r = 0; r < R; ++r) q[r] = op[r];
   auto load_col = [&](int u, T (&dst)[R]) {
-    const long long col = c0 + u;
+    const IdxT col = c0 + u;
     if (!EDGE || FIRST || (has_in && col < len)) {
 #pragma unroll
       for (int r = 0; r < R; ++r) dst[r] = islot[LEFT ? (lane + 32 * r) * (K + 1) + u : u * TR + lane + 32 * r];
@@ -644,7 +648,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
     if (u < K) load_col(u + 1, nxt);
     // outgoing column (LEFT may stage it in place of the column just read)
     if (has_out) {
-      const long long col = c0 - (K + 1) + u;
+      const IdxT col = c0 - (K + 1) + u;
       if (!EDGE || col < len) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -667,7 +671,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
         }
       }
       if constexpr (EDGE && !FIRST) {
-        if (final_exit && col == (long long)len - 1) {  // the unit's last column is out
+        if (final_exit && col == (IdxT)len - 1) {  // the unit's last column is out
           if (early_out != nullptr) {
             __syncwarp();
             if (lane == 0) mbar_arrive(early_out);
@@ -687,8 +691,8 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
         if (l >= u) continue;  // j = u - 1 - l < 0 (compile time)
         if (l >= Kb) continue;
       } else if (EDGE) {
-        const long long j = c0 + u - 1 - l;
-        if (l >= Kb || j < 0 || j > (long long)len - 2) continue;
+        const IdxT j = c0 + u - 1 - l;
+        if (l >= Kb || j < 0 || j > (IdxT)len - 2) continue;
       }
       // interior blocks: the record of step t = u*NL + l was loaded CD steps earlier
       CoefT cf;

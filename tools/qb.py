@@ -30,10 +30,15 @@ def bench(name, reps):
         torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
     f = flops_applied(m, n, k, Side(side))
     ts.sort()
-    print(f"{os.environ.get('RS_LIB_PATH', 'default').split('/')[-1]:>24} {name}: best {ts[0]:.4f} ms median {ts[len(ts)//2]:.4f} ms"
+    info = _lib.plan_info(m, n, k, 1 if side == "left" else 0, 0, 0 if dtype == torch.float64 else 1)
+    print(f"{os.environ.get('RS_LIB_PATH', 'default').split('/')[-1]:>12} {info['grid_ctas']}x{info['warps_per_cta']}w u={info['units']} {name}: best {ts[0]:.4f} ms median {ts[len(ts)//2]:.4f} ms"
           f" -> {f/ts[0]/1e9:.2f} / {f/ts[len(ts)//2]/1e9:.2f} TF/s (step incl. pack)", flush=True)
 
 
+for a in sys.argv[1:]:
+    if a.count("x") == 2 and a.replace("x", "").isdigit():
+        mm, nn, kk = (int(v) for v in a.split("x"))
+        CFG[a] = (mm, nn, kk, torch.float64, "right", "forward")
 names = [a for a in sys.argv[1:] if a in CFG]
 reps = next((int(a) for a in sys.argv[1:] if a.isdigit()), 20)
 for nm in names or ["c2"]:
