@@ -177,7 +177,9 @@ struct LaunchPlan {
   long long units = 0;
   int ua = 0;
   long long t1 = 0;
-  int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units; 3: aligned
+  int mode = 1;  // 1: few units per SMSP (mixed widths); 2: full-width units; 3: aligned;
+                 // 4: equal chains of mixed widths on more SMs than the aligned plan
+  int sweep_off = 0;  // offset of the sweep split (sweep_start)
 };
 
 size_t smem_per_warp(size_t tsz, size_t coef_rec, bool left, int K, bool refl) {
@@ -247,6 +249,86 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
         const long long G2 = cr / r;
         if (G2 * 5 < grid * 4) continue;
         if (G2 > bestG) bestG = G2, bestU = U, bestNW = nw;
+      }
+    }
+    // Equal-chain plan: when the aligned plan runs a single round on fewer SMs than the
+    // device has, chains of ut' > ut units (widths floor/ceil of k/ut', the wider ones placed
+    // mid-period by sweep_off = ut'/2, away from the chain's tail and from most flag
+    // hand-offs) can fill more SMs with one unit per warp: every chain identical, every
+    // sub-partition within one sweep of the others. Taken when the modelled time
+    //   (blocks + 2.2 per ring hop + 9 per CTA crossing) x (sweeps per sub-partition)
+    // beats the aligned plan's by 2% (measured, B200, config 2: 144 CTAs x 12 warps, 27
+    // units of 7-8 sweeps per tile, 19.1 vs 18.7 TF/s; with the wide units last, as
+    // sweep_off = 0 puts them, the same plan gives 18.3).
+    // Only where the aligned chains already cross CTAs (ut > nw): a chain that fits one
+    // CTA has no flag hand-off at all, and giving it some costs more than the extra SMs
+    // return (measured, config 4: 30.2 vs 32.9 TF/s).
+    if (bestG > 0 && bestG < grid && bestU / bestNW == bestG && bestU / g.tiles > bestNW &&
+        !getenv("RS_NO_EQUAL_CHAIN")) {
+      const int ut_a = (int)(bestU / g.tiles);
+      auto cost = [&](int ut, int nw, int per_smsp_sweeps) {
+        const double cross = (double)((ut + nw - 1) / nw - 1) + (ut % nw ? 0.5 : 0.0);
+        return ((double)g.nblk + 2.2 * (ut - 1) + 9.0 * cross) * per_smsp_sweeps;
+      };
+      const double cost_a = cost(ut_a, bestNW, (bestNW / 4) * (g.k / ut_a));
+      double best_c = 0.98 * cost_a;
+      long long eG = 0, eU = 0;
+      int eNW = 0;
+      for (int ut = ut_a + 1; ut <= ut_a + ut_a / 4 && ut <= g.k; ++ut) {
+        if (g.k % ut == 0 || g.k / ut < 2) continue;  // uniform widths are the aligned plan's
+        const long long U = g.tiles * ut;
+        for (int nw = cap; nw >= 8; nw -= 4) {
+          if (U % nw != 0) continue;
+          const long long G2 = U / nw;
+          if (G2 > grid || G2 <= bestG) continue;
+          // per sub-partition: nw/4 units of floor(k/ut) sweeps and at most one wider one
+          // (the wide units are at least 4 chain positions apart when k % ut <= ut / 4)
+          if ((long long)(g.k % ut) * 4 > ut) continue;
+          const double c = cost(ut, nw, (nw / 4) * (g.k / ut) + 1);
+          if (c < best_c) best_c = c, eG = G2, eU = U, eNW = nw;
+        }
+      }
+      if (eG > 0) {
+        lp->grid = (int)eG;
+        lp->nw = eNW;
+        lp->smem = per * eNW + ctl;
+        lp->units = eU;
+        lp->mode = 4;
+        lp->ua = (int)(eU / g.tiles);
+        lp->t1 = 0;
+        // the offset whose wide units fall least often on a chain's head, tail or flag
+        // hand-off units (first / last unit of a CTA's range), over the tiles' phases
+        // against the CTA boundaries (config 2: offsets 3-5, wide units at 7, 16, 25 of 27:
+        // 19.3 TF/s; 9 -> 18.4, 18 -> 18.6, where they meet the flag units)
+        // (memoised: the search is ~9000 steps of host time on every launch otherwise)
+        struct OffMemo { int ut = 0, nw = 0, k = 0, off = 0; };
+        static thread_local OffMemo memo;
+        if (memo.ut == lp->ua && memo.nw == eNW && memo.k == g.k) {
+          lp->sweep_off = memo.off;
+        } else {
+          const int ut = lp->ua, nw = eNW, w0 = g.k / ut;
+          int best_off = 0;
+          long long best_score = -1;
+          for (int off = 0; off < ut; ++off) {
+            long long score = 0;
+            for (int t = 0; t < nw; ++t) {  // phases repeat with period <= nw tiles
+              const int phase = (int)(((long long)t * ut) % nw);
+              for (int i = 0; i < ut; ++i) {
+                if (sweep_start(i + 1, ut, g.k, off) - sweep_start(i, ut, g.k, off) <= w0) continue;
+                const int pos = (phase + i) % nw;
+                if (i == 0 || i == ut - 1 || pos == 0 || pos == nw - 1) ++score;
+              }
+            }
+            if (best_score < 0 || score < best_score) best_score = score, best_off = off;
+          }
+          lp->sweep_off = best_off;
+          memo.ut = ut, memo.nw = nw, memo.k = g.k, memo.off = best_off;
+        }
+        if (const char* ev = getenv("RS_SWEEP_OFF")) {
+          const int v = atoi(ev);
+          if (v >= 0 && v < lp->ua) lp->sweep_off = v;
+        }
+        return RS_OK;
       }
     }
     if (bestG > 0) {
@@ -343,19 +425,19 @@ rs_status launch_pack(const Geometry& g, const T* C, const T* S, long long ldcs,
     SCoef<T>* const sout = reinterpret_cast<SCoef<T>*>(base + g.std_bytes);
     if (g.kw == wide_k(sizeof(T)))
       rs_pack_scaled_kernel<T, REFL, wide_k(sizeof(T))><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua,
-                                                                    nparts, rev, unsafe);
+                                                                    nparts, rev, unsafe, lp.sweep_off);
     else
       rs_pack_scaled_kernel<T, REFL, kK><<<sgrid, 128, 0, st>>>(sout, C, S, ldcs, g.len, g.k, g.nblk, lp.ua, nparts,
-                                                                rev, unsafe);
+                                                                rev, unsafe, lp.sweep_off);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   const uint32_t* const only = scaled && std_only_if_unsafe ? unsafe : nullptr;
   if (g.kw == wide_k(sizeof(T)))
     rs_pack_kernel<T, REFL, wide_k(sizeof(T))><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
-                                                                                      g.nblk, lp.ua, nparts, rev, only);
+                                                                                      g.nblk, lp.ua, nparts, rev, only, lp.sweep_off);
   else
     rs_pack_kernel<T, REFL, kK><<<dim3((unsigned)bx, (unsigned)by), 256, 0, st>>>(coef, C, S, ldcs, g.len, g.k,
-                                                                                  g.nblk, lp.ua, nparts, rev, only);
+                                                                                  g.nblk, lp.ua, nparts, rev, only, lp.sweep_off);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("pack launch: ") + cudaGetErrorString(e));
@@ -408,6 +490,7 @@ rs_status launch_run(const Geometry& g, T* Abase, int rev, void* ws, cudaStream_
     const int v = atoi(ev);
     if (v >= 1 && v <= stages_for(sizeof(T))) P.credit = v;
   }
+  P.sweep_off = lp.sweep_off;
   P.len = g.len;
   P.k = g.k;
   P.nchunk = g.nchunk;

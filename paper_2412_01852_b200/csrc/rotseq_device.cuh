@@ -477,6 +477,7 @@ struct PipeParams {
   int cw;                   // chunk width in wave columns
   int ncw;                  // number of chunks
   unsigned long long* trace;  // debug timeline buffer (RS_TRACE builds), or null
+  int sweep_off;     // offset of the sweep split (sweep_start), 0 <= sweep_off < units per tile
 };
 
 // ------------------------------------------------------------------------------------
@@ -494,13 +495,19 @@ struct Unit {
 // First sweep of unit i (of ut) of a tile: the k sweeps split evenly. (Uneven splits —
 // a narrower head unit, widths tapered along the chain — measured much slower: a chain
 // runs at the pace of its widest unit.)
-__host__ __device__ __forceinline__ int sweep_start(long long i, int ut, int k) {
-  return (int)(i * k / ut);
+// `off` (0 <= off < ut) shifts where the wider units of an uneven split fall inside a chain
+// (the ends stay 0 and k): with off = 0 the wider unit of each period comes last, which
+// puts one on the chain's tail and, for some tiles, on the units that also carry a
+// flag hand-off; the equal-chain plans (plan_launch) use off = ut/2.
+__host__ __device__ __forceinline__ int sweep_start(long long i, int ut, int k, int off = 0) {
+  if (i <= 0) return 0;
+  if (i >= ut) return k;
+  return (int)((i * k + off) / ut);
 }
 __host__ __device__ __forceinline__ long long tile_first_unit(long long t, long long t1, int ua) {
   return t < t1 ? t * (ua + 1) : t1 * (ua + 1) + (t - t1) * ua;
 }
-__host__ __device__ __forceinline__ Unit unit_at(long long g, long long t1, int ua, int k) {
+__host__ __device__ __forceinline__ Unit unit_at(long long g, long long t1, int ua, int k, int off = 0) {
   Unit u;
   const long long big = t1 * (ua + 1);
   long long i;
@@ -515,8 +522,8 @@ __host__ __device__ __forceinline__ Unit unit_at(long long g, long long t1, int 
     i = r - (u.tile - t1) * ua;
     ut = ua;
   }
-  u.p0 = sweep_start(i, ut, k);
-  u.kb = sweep_start(i + 1, ut, k) - u.p0;
+  u.p0 = sweep_start(i, ut, k, off);
+  u.kb = sweep_start(i + 1, ut, k, off) - u.p0;
   return u;
 }
 // CTA c runs units [g0, g1). When the range ends inside a tile whose first unit lies inside
@@ -526,13 +533,13 @@ struct CtaRange {
   int nl;
 };
 __host__ __device__ __forceinline__ CtaRange cta_range(long long U, long long c, long long G, long long t1, int ua,
-                                                       int k) {
+                                                       int k, int off = 0) {
   CtaRange r;
   r.g0 = U * c / G;
   r.g1 = U * (c + 1) / G;
   r.nl = 0;
   if (r.g1 > r.g0) {
-    const Unit last = unit_at(r.g1 - 1, t1, ua, k);
+    const Unit last = unit_at(r.g1 - 1, t1, ua, k, off);
     if (last.p0 + last.kb < k) {
       const long long f = tile_first_unit(last.tile, t1, ua);
       if (f > r.g0) r.nl = (int)(r.g1 - f);
@@ -770,7 +777,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
   const uint32_t fullin_a = smem_u32(full_in), fullout_a = smem_u32(full_out);
   const uint32_t consin_a = smem_u32(consumed_in), cbar_a = smem_u32(cbar), cbuf_a = smem_u32(cbuf);
 
-  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
+  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k, P.sweep_off);
   const long long npos = cr.g1 - cr.g0;
   uint32_t cseq = 0;  // coefficient blocks consumed by this warp (buffer = cseq&1)
 
@@ -778,7 +785,7 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
     const long long pos = (long long)jr * NW + slot;
     if (pos >= npos) break;
     const long long g = pos_to_unit(cr, pos);
-    const Unit un = unit_at(g, P.t1, P.ua, k);
+    const Unit un = unit_at(g, P.t1, P.ua, k, P.sweep_off);
     const long long tile = un.tile;
     const int p0 = un.p0;
     const int Kb = un.kb;
@@ -1153,7 +1160,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
   T* const rout = ring_sm + (size_t)(warp + 1) * S * CHUNK;
   unsigned char* const cbuf = smem_raw + (size_t)warp * 2 * coef_blocks_per_buf(LEFT) * CBUF;
 
-  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k);
+  const CtaRange cr = cta_range(P.units, blockIdx.x, gridDim.x, P.t1, P.ua, k, P.sweep_off);
   const long long npos = cr.g1 - cr.g0;
   uint32_t cseq = 0;  // coefficient block pairs consumed by this warp (buffer = cseq&1)
 
@@ -1161,7 +1168,7 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
     const long long pos = (long long)jr * NW + slot;
     if (pos >= npos) break;
     const long long g = pos_to_unit(cr, pos);
-    const Unit un = unit_at(g, P.t1, P.ua, k);
+    const Unit un = unit_at(g, P.t1, P.ua, k, P.sweep_off);
     const long long tile = un.tile;
     const int p0 = un.p0;
     const int Kb = un.kb;
@@ -1567,7 +1574,7 @@ template <typename T, bool REFL, int K>
 __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict__ out, const T* __restrict__ C,
                                                       const T* __restrict__ Sm, long long ldcs, int len, int k,
                                                       int nblk, int ua, int nparts, int rev,
-                                                      const uint32_t* __restrict__ only_if_unsafe) {
+                                                      const uint32_t* __restrict__ only_if_unsafe, int off) {
   const int per_p = nblk * (K + 1);
   for (int row = blockIdx.y; row < nparts * k; row += gridDim.y) {
     const int part = row / k;
@@ -1575,13 +1582,13 @@ __global__ void __launch_bounds__(256) rs_pack_kernel(Coef<T, REFL>* __restrict_
     const int ut = ua + part;
     // unit i of this partition holding sweep p: p0(i) = floor(i*k/ut)
     int i = (int)(((long long)p * ut) / k);
-    while (i + 1 < ut && sweep_start(i + 1, ut, k) <= p) ++i;
-    while (i > 0 && sweep_start(i, ut, k) > p) --i;
+    while (i + 1 < ut && sweep_start(i + 1, ut, k, off) <= p) ++i;
+    while (i > 0 && sweep_start(i, ut, k, off) > p) --i;
     // fast mode packs the scaled records first; the standard records are only the
     // fallback of the units whose coefficients are outside the scaled form's safe range
     if (only_if_unsafe != nullptr && only_if_unsafe[part * (ua + 1) + i] == 0u) continue;
-    const int p0 = sweep_start(i, ut, k);
-    const int kb = sweep_start(i + 1, ut, k) - p0;
+    const int p0 = sweep_start(i, ut, k, off);
+    const int kb = sweep_start(i + 1, ut, k, off) - p0;
     const int l = p - p0;
     constexpr bool PAIR = kPairRecs<T, REFL>;
     const int nr = recs_per_wave(kb, PAIR);
@@ -1636,7 +1643,7 @@ template <typename T, bool REFL, int K>
 __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restrict__ out, const T* __restrict__ C,
                                                              const T* __restrict__ Sm, long long ldcs, int len, int k,
                                                              int nblk, int ua, int nparts, int rev,
-                                                             uint32_t* __restrict__ unsafe) {
+                                                             uint32_t* __restrict__ unsafe, int off) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= len) return;
   // scales and taus are formed in fp64 (for fp32 too) and rounded once when stored
@@ -1660,8 +1667,8 @@ __global__ void __launch_bounds__(256) rs_pack_scaled_kernel(SCoef<T>* __restric
     const int i = row - part * (ua + 1);  // unit index within the tile
     const int ut = ua + part;
     if (i >= ut) continue;
-    const int p0 = sweep_start(i, ut, k);
-    const int kb = sweep_start(i + 1, ut, k) - p0;
+    const int p0 = sweep_start(i, ut, k, off);
+    const int kb = sweep_start(i + 1, ut, k, off) - p0;
     constexpr bool PAIR = kPairRecs<T, REFL>;
     const int nr = recs_per_wave(kb, PAIR);
     constexpr int SR = scale_recs(K, sizeof(T));

@@ -51,8 +51,62 @@ def warp_cap(dtype_bytes: int = 8, refl: bool = False, R: int = 2, K: int = 8, S
     return min(max_warps, (optin - (S + 3) * 8) // per) & ~3
 
 
-def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mode: int = 0):
-    """plan_launch(): grid, U, ua, t1, NW."""
+def equal_chain_plan(g: Geometry, grid: int, cap: int, bestG: int, bestU: int, bestNW: int):
+    """plan_launch()'s equal-chain candidate: one round, chains of ut' > ut units of mixed
+    widths on more SMs than the aligned plan, wide units mid-period (off = ut' // 2)."""
+    if not (bestG < grid and bestU // bestNW == bestG and bestU // g.tiles > bestNW):
+        return None
+    ut_a = bestU // g.tiles
+
+    def cost(ut, nw, per_smsp):
+        cross = (-(-ut // nw) - 1) + (0.5 if ut % nw else 0.0)
+        return (g.nblk + 2.2 * (ut - 1) + 9.0 * cross) * per_smsp
+
+    best_c = 0.98 * cost(ut_a, bestNW, (bestNW // 4) * (g.k // ut_a))
+    pick = None
+    for ut in range(ut_a + 1, min(ut_a + ut_a // 4, g.k) + 1):
+        if g.k % ut == 0 or g.k // ut < 2:
+            continue
+        U = g.tiles * ut
+        for nw in range(cap, 7, -4):
+            if U % nw:
+                continue
+            G2 = U // nw
+            if G2 > grid or G2 <= bestG or (g.k % ut) * 4 > ut:
+                continue
+            c = cost(ut, nw, (nw // 4) * (g.k // ut) + 1)
+            if c < best_c:
+                best_c, pick = c, (G2, U, nw)
+    if pick is None:
+        return None
+    G2, U, nw = pick
+    ua = U // g.tiles
+    return dict(G=G2, U=U, ua=ua, t1=0, NW=nw, off=best_sweep_offset(ua, nw, g.k))
+
+
+def best_sweep_offset(ut: int, nw: int, k: int) -> int:
+    """The offset whose wide units fall least often on a chain's head, tail or flag hand-off
+    units (first / last unit of a CTA's range) over the tiles' phases; smallest on ties."""
+    w0 = k // ut
+    best = None
+    for off in range(ut):
+        score = 0
+        for t in range(nw):
+            phase = (t * ut) % nw
+            for i in range(ut):
+                if sweep_start(i + 1, ut, k, off) - sweep_start(i, ut, k, off) <= w0:
+                    continue
+                pos = (phase + i) % nw
+                if i == 0 or i == ut - 1 or pos == 0 or pos == nw - 1:
+                    score += 1
+        if best is None or score < best[0]:
+            best = (score, off)
+    return best[1]
+
+
+def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mode: int = 0,
+         equal_chain: bool = True):
+    """plan_launch(): grid, U, ua, t1, NW, off (sweep-split offset)."""
     cap = max(4, cap & ~3)
     G = sms if grid is None else min(grid, sms)
     if mode in (0, 3) and grid is None:
@@ -79,7 +133,10 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
                     best = (G2, U, nw)
         if best is not None:
             G2, U, nw = best
-            return dict(G=G2, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw)
+            eq = equal_chain_plan(g, G, cap, G2, U, nw) if equal_chain else None
+            if eq is not None:
+                return eq
+            return dict(G=G2, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw, off=0)
     umin = g.tiles * -(-g.k // g.K)
     G = max(1, min(G, -(-umin // 4)))
     q = -(-umin // (4 * G))
@@ -91,29 +148,33 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
     nmax = -(-U // G)
     rounds = -(-nmax // cap)
     nw = min(cap, -(-(-(-nmax // rounds)) // 4) * 4)
-    return dict(G=G, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw)
+    return dict(G=G, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw, off=0)
 
 
 def tile_first_unit(t, t1, ua):
     return t * (ua + 1) if t < t1 else t1 * (ua + 1) + (t - t1) * ua
 
 
-def unit_at(gidx, t1, ua, k):
+def sweep_start(i, ut, k, off=0):
+    return 0 if i <= 0 else k if i >= ut else (i * k + off) // ut
+
+
+def unit_at(gidx, t1, ua, k, off=0):
     big = t1 * (ua + 1)
     if gidx < big:
         tile, i, ut = gidx // (ua + 1), gidx % (ua + 1), ua + 1
     else:
         r = gidx - big
         tile, i, ut = t1 + r // ua, r % ua, ua
-    p0 = i * k // ut
-    return tile, p0, (i + 1) * k // ut - p0
+    p0 = sweep_start(i, ut, k, off)
+    return tile, p0, sweep_start(i + 1, ut, k, off) - p0
 
 
-def cta_range(U, c, G, t1, ua, k):
+def cta_range(U, c, G, t1, ua, k, off=0):
     g0, g1 = U * c // G, U * (c + 1) // G
     nl = 0
     if g1 > g0:
-        tile, p0, kb = unit_at(g1 - 1, t1, ua, k)
+        tile, p0, kb = unit_at(g1 - 1, t1, ua, k, off)
         if p0 + kb < k:
             f = tile_first_unit(tile, t1, ua)
             if f > g0:
@@ -124,7 +185,8 @@ def cta_range(U, c, G, t1, ua, k):
 def cta_schedule(g: Geometry, pl: dict, c: int):
     """List of (pos, warp, round, unit gidx, (tile, p0, kb), src, dst) for CTA c."""
     U, G, t1, ua, NW, k = pl["U"], pl["G"], pl["t1"], pl["ua"], pl["NW"], g.k
-    g0, g1, nl = cta_range(U, c, G, t1, ua, k)
+    off = pl.get("off", 0)
+    g0, g1, nl = cta_range(U, c, G, t1, ua, k, off)
 
     def pos_to_unit(p):
         return g1 - nl + p if p < nl else g0 + p - nl
@@ -136,7 +198,7 @@ def cta_schedule(g: Geometry, pl: dict, c: int):
     for p in range(g1 - g0):
         w, jr = p % NW, p // NW
         u = pos_to_unit(p)
-        tile, p0, kb = unit_at(u, t1, ua, k)
+        tile, p0, kb = unit_at(u, t1, ua, k, off)
         src = "global"
         if p0 > 0:
             src = "ring" if (w > 0 and u - 1 >= g0 and unit_to_pos(u - 1) == p - 1) else "flag"

@@ -165,3 +165,47 @@ def test_aligned_plans_bitwise_vs_naive_kernel(cuda, m, n, k, side):
     apply_device(B, (C, S), fast=False, side=side, algo="naive")
     torch.cuda.synchronize()
     assert_bitwise(B.cpu().numpy(), A.cpu().numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ("rotation", "reflector"))
+def test_equal_chain_plan_bitwise_and_fast_tolerance(cuda, kind):
+    """The equal-chain plan (chains of 27 units of 7-8 sweeps on 144 CTAs, sweep-split
+    offset; what config 2's shape selects on a 148-SM B200) against the independent
+    one-thread-per-owner kernel: strict bitwise, fast within 10 k eps; and with the plan
+    switched off (RS_NO_EQUAL_CHAIN=1: the aligned plan) bit-identical strict results."""
+    import os
+
+    import torch
+
+    from paper_2412_01852_b200 import _lib, apply_device
+
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("the plan under test is chosen for a 148-SM B200")
+    m, n, k = 4096, 2304, 192   # 64 tiles x 192 sweeps: the same unit split as config 2
+    info = _lib.plan_info(m, n, k)
+    assert (info["grid_ctas"], info["warps_per_cta"], info["units"]) == (144, 12, 1728)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    A0 = torch.randn(n, m, dtype=torch.float64, generator=g).to(cuda).t()
+    th = torch.rand(k, n - 1, dtype=torch.float64, generator=g).t() * 6.283185307179586
+    C, S = torch.cos(th).to(cuda), torch.sin(th).to(cuda)
+    ref = A0.clone(memory_format=torch.preserve_format)
+    apply_device(ref, (C, S), fast=False, kind=kind, algo="naive")
+    got = A0.clone(memory_format=torch.preserve_format)
+    apply_device(got, (C, S), fast=False, kind=kind)
+    torch.cuda.synchronize()
+    assert_bitwise(ref.cpu().numpy(), got.cpu().numpy())
+    fast = A0.clone(memory_format=torch.preserve_format)
+    apply_device(fast, (C, S), fast=True, kind=kind)
+    torch.cuda.synchronize()
+    rel = (torch.linalg.norm(fast - ref) / torch.linalg.norm(ref)).item()
+    assert rel <= 10 * k * 2.220446049250313e-16, rel
+    os.environ["RS_NO_EQUAL_CHAIN"] = "1"
+    try:
+        assert _lib.plan_info(m, n, k)["grid_ctas"] == 128
+        alt = A0.clone(memory_format=torch.preserve_format)
+        apply_device(alt, (C, S), fast=False, kind=kind)
+        torch.cuda.synchronize()
+    finally:
+        del os.environ["RS_NO_EQUAL_CHAIN"]
+    assert_bitwise(ref.cpu().numpy(), alt.cpu().numpy())

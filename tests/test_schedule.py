@@ -142,7 +142,7 @@ def test_kernel_emulator_golden(golden):
 
 
 @pytest.mark.parametrize("owners,length,k,cap,expect", [
-    (4096, 4096, 192, 16, dict(G=128, NW=12, U=1536)),     # config 2: 2 CTAs per tile chain
+    (4096, 4096, 192, 16, dict(G=144, NW=12, U=1728)),     # config 2: equal chains of 27 units (7-8 sweeps)
     (8192, 8192, 128, 16, dict(G=128, NW=16, U=2048)),     # config 4: 1 CTA per chain
     (16384, 16384, 96, 12, dict(G=128, NW=12, U=3072)),    # config 5: 2 rounds, 1 chain each
     (65536, 2048, 256, 16, dict(G=148, NW=16, U=32768)),   # config 3: many rounds keep all SMs
@@ -155,6 +155,34 @@ def test_aligned_plans_for_baseline_configs(owners, length, k, cap, expect):
     assert {key: pl[key] for key in expect} == expect
     if pl["G"] == 128:
         assert pl["t1"] == 0 and k % pl["ua"] == 0  # every unit exactly k/ut sweeps wide
+
+
+def test_equal_chain_plan_for_config_2():
+    """Config 2: the aligned plan (24 units of 8 sweeps, 128 CTAs, chains crossing CTAs) gives
+    way to equal chains of 27 units on 144 CTAs; the three 8-sweep units of a chain sit at
+    positions 7, 16, 25 — never the head, the tail or a flag hand-off unit of any tile."""
+    from pipeline_model import cta_schedule, unit_at
+    g = Geometry(owners=4096, length=4096, k=192)
+    aligned = plan(g, cap=16, equal_chain=False)
+    assert (aligned["G"], aligned["NW"], aligned["U"], aligned["off"]) == (128, 12, 1536, 0)
+    pl = plan(g, cap=16)
+    assert (pl["G"], pl["NW"], pl["U"], pl["ua"], pl["t1"]) == (144, 12, 1728, 27, 0)
+    widths = [unit_at(i, 0, 27, 192, pl["off"])[2] for i in range(27)]
+    assert sum(widths) == 192 and [i for i, w in enumerate(widths) if w == 8] == [7, 16, 25]
+    for c in range(pl["G"]):
+        loads = [0, 0, 0, 0]
+        for _, w, _, _, (_, p0, kb), src, dst in cta_schedule(g, pl, c):
+            loads[w % 4] += kb
+            if kb == 8:  # a wide unit is a plain ring-to-ring stage
+                assert (src, dst) == ("ring", "ring")
+        assert max(loads) <= 22 and min(loads) >= 21, loads
+    # a chain that fits one CTA keeps its aligned plan (config 4: no flag hand-off to add)
+    assert plan(Geometry(owners=8192, length=8192, k=128), cap=16)["G"] == 128
+
+
+def test_equal_chain_plan_protocol_is_deadlock_free():
+    res = simulate(Geometry(owners=1024, length=2100, k=192), sms=37, cap=16)
+    assert (res["plan"]["G"], res["plan"]["ua"]) == (36, 27)
 
 
 @pytest.mark.parametrize("owners,length,k,cap", [(16384, 16384, 96, 12), (16384, 2048, 256, 16)])
