@@ -274,16 +274,22 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
       double best_c = 0.98 * cost_a;
       long long eG = 0, eU = 0;
       int eNW = 0;
-      for (int ut = ut_a + 1; ut <= ut_a + ut_a / 4 && ut <= g.k; ++ut) {
+      // developer knobs (measurements): force the chain length / warps per CTA
+      const int force_eut = getenv("RS_EQ_UT") ? atoi(getenv("RS_EQ_UT")) : 0;
+      const int force_enw = getenv("RS_EQ_NW") ? atoi(getenv("RS_EQ_NW")) : 0;
+      if (force_eut > 0) best_c = 1e300;
+      for (int ut = ut_a + 1; (ut <= ut_a + ut_a / 4 || force_eut > 0) && ut <= g.k; ++ut) {
+        if (force_eut > 0 && ut != force_eut) continue;
         if (g.k % ut == 0 || g.k / ut < 2) continue;  // uniform widths are the aligned plan's
         const long long U = g.tiles * ut;
         for (int nw = cap; nw >= 8; nw -= 4) {
+          if (force_enw > 0 && nw != force_enw) continue;
           if (U % nw != 0) continue;
           const long long G2 = U / nw;
           if (G2 > grid || G2 <= bestG) continue;
           // per sub-partition: nw/4 units of floor(k/ut) sweeps and at most one wider one
           // (the wide units are at least 4 chain positions apart when k % ut <= ut / 4)
-          if ((long long)(g.k % ut) * 4 > ut) continue;
+          if ((long long)(g.k % ut) * 4 > ut && force_eut == 0) continue;
           const double c = cost(ut, nw, (nw / 4) * (g.k / ut) + 1);
           if (c < best_c) best_c = c, eG = G2, eU = U, eNW = nw;
         }
