@@ -636,7 +636,10 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   // coefficient records prefetched CD rotation steps ahead (register queue; the ring index
   // t % CD is a compile-time constant in the unrolled loops)
   using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
-  constexpr int CD = 4;
+#ifndef RS_COEF_QUEUE
+#define RS_COEF_QUEUE 4
+#endif
+  constexpr int CD = RS_COEF_QUEUE;
   CoefT cq[CD];
   if constexpr (!EDGE) {
 #pragma unroll
