@@ -589,8 +589,17 @@ __device__ __forceinline__ void dispatch_width(int Kb, F&& f) {
 // len-1; when `early_out` is set (ring output) the consumer's "full" barrier is signalled
 // right there, and the rest of the block (rotations that are all out of range) is skipped.
 // Both shorten the hand-off lag per chain hop.
+// CDQ: depth of the register queue of prefetched coefficient records. 4 everywhere except the
+// 168-register fp64 right-side build, where 6 measures +2.3% (config 2: 19.4 -> 19.9 TF/s per
+// step; 2 / 3 / 8: 19.7 / 19.5 / 19.7) — and -2.5% on the 128-register build (config 3).
+#ifndef RS_COEF_QUEUE
+#define RS_COEF_QUEUE 4
+#endif
+#ifndef RS_COEF_QUEUE_SMALL
+#define RS_COEF_QUEUE_SMALL 6
+#endif
 template <typename T, int K, int R, int KB, bool STRICT, bool REFL, bool EDGE, bool SCALED, bool LEFT, bool OUTS,
-          bool FIRST = false>
+          bool FIRST = false, int CDQ = RS_COEF_QUEUE>
 __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
                                           const std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>* __restrict__ cb,
                                           const T* islot, T* const (&op)[R], const long long (&ostr)[R],
@@ -636,10 +645,7 @@ __device__ __forceinline__ void run_block(T (&w)[R][K + 1],
   // coefficient records prefetched CD rotation steps ahead (register queue; the ring index
   // t % CD is a compile-time constant in the unrolled loops)
   using CoefT = std::conditional_t<SCALED, SCoef<T>, Coef<T, REFL>>;
-#ifndef RS_COEF_QUEUE
-#define RS_COEF_QUEUE 4
-#endif
-  constexpr int CD = RS_COEF_QUEUE;
+  constexpr int CD = CDQ;
   CoefT cq[CD];
   if constexpr (!EDGE) {
 #pragma unroll
@@ -1125,7 +1131,8 @@ __device__ __forceinline__ void pipeline_units(const PipeParams& P, unsigned cha
 // Right side: the original per-block protocol (generic-pointer output, lane-0 branches);
 // it schedules the unrolled body better than the lean protocol under the 128-register
 // budget of 16-warp CTAs.
-template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED_ANY, bool HS, bool LEFT>
+template <typename T, int K, int R, bool STRICT, bool REFL, bool SCALED_ANY, bool HS, bool LEFT,
+          int CDQ = RS_COEF_QUEUE>
 __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsigned char* smem_raw) {
   static_assert(!LEFT, "right-side protocol");
   constexpr int TR = 32 * R;
@@ -1407,11 +1414,11 @@ __device__ __forceinline__ void pipeline_units_right(const PipeParams& P, unsign
 #endif
           // the draining last block signals the consumer at its final column and stops there
           uint64_t* const early = (SUB == 1 && b == nblk - 1) ? &full_out[oseq % S] : nullptr;
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true, FIRST>(
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, true, FIRST, CDQ>(
               w, cbp, islot, op, ostr, obase_s, b, len, Kb, lane, b < nchunk, b >= 1, sub_in, sub_par, sub_out,
               b == nblk - 1, early);
         } else {
-          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false, FIRST>(
+          run_block<T, K, R, KB, STRICT, REFL, EDGE, SCALED, LEFT, false, FIRST, CDQ>(
               w, cbp, islot, op, ostr, nullptr, b, len, Kb, lane, b < nchunk, b >= 1, sub_in, sub_par, sub_out,
               b == nblk - 1, nullptr);
         }
@@ -1528,6 +1535,8 @@ __global__ void __launch_bounds__(MW * 32, 1) rs_pipeline_kernel(const __grid_co
   constexpr int S = stages_for(sizeof(T));
   constexpr int NBAR = ctl_words(S, LEFT);
   constexpr size_t CBUF = coef_buf_bytes<T, REFL, K>();
+  // the 168-register build (fp64 right side, <= 12 warps) affords a deeper coefficient queue
+  constexpr int CDQ = (sizeof(T) == 8 && !LEFT && MW <= 12 && K == kK) ? RS_COEF_QUEUE_SMALL : RS_COEF_QUEUE;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NW = P.nw;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * 2 * coef_blocks_per_buf(LEFT) * CBUF +
@@ -1552,7 +1561,7 @@ __global__ void __launch_bounds__(MW * 32, 1) rs_pipeline_kernel(const __grid_co
       if constexpr (LEFT || RS_RIGHT_LEAN) {
         pipeline_units<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
       } else {
-        pipeline_units_right<T, K, R, STRICT, REFL, true, HS, LEFT>(P, smem_raw);
+        pipeline_units_right<T, K, R, STRICT, REFL, true, HS, LEFT, CDQ>(P, smem_raw);
       }
       return;
     }
@@ -1560,7 +1569,7 @@ __global__ void __launch_bounds__(MW * 32, 1) rs_pipeline_kernel(const __grid_co
   if constexpr (LEFT || RS_RIGHT_LEAN) {
     pipeline_units<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
   } else {
-    pipeline_units_right<T, K, R, STRICT, REFL, false, HS, LEFT>(P, smem_raw);
+    pipeline_units_right<T, K, R, STRICT, REFL, false, HS, LEFT, CDQ>(P, smem_raw);
   }
 }
 
