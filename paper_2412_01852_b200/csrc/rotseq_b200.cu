@@ -263,7 +263,9 @@ rs_status plan_launch(const Geometry& g, size_t tsz, LaunchPlan* lp) {
     // Only where the aligned chains already cross CTAs (ut > nw): a chain that fits one
     // CTA has no flag hand-off at all, and giving it some costs more than the extra SMs
     // return (measured, config 4: 30.2 vs 32.9 TF/s).
-    if (bestG > 0 && bestG < grid && bestU / bestNW == bestG && bestU / g.tiles > bestNW &&
+    // Right side only: the left-side protocol lacks the shorter unit edges and loses with the
+    // longer chains (4096^2, k = 192, left / reverse: 16.8 vs 17.6 TF/s).
+    if (bestG > 0 && bestG < grid && bestU / bestNW == bestG && bestU / g.tiles > bestNW && !g.left &&
         !getenv("RS_NO_EQUAL_CHAIN")) {
       const int ut_a = (int)(bestU / g.tiles);
       auto cost = [&](int ut, int nw, int per_smsp_sweeps) {

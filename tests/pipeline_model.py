@@ -105,7 +105,7 @@ def best_sweep_offset(ut: int, nw: int, k: int) -> int:
 
 
 def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mode: int = 0,
-         equal_chain: bool = True):
+         equal_chain: bool = True, left: bool = False):
     """plan_launch(): grid, U, ua, t1, NW, off (sweep-split offset)."""
     cap = max(4, cap & ~3)
     G = sms if grid is None else min(grid, sms)
@@ -133,7 +133,7 @@ def plan(g: Geometry, sms: int = 148, cap: int = 16, grid: int | None = None, mo
                     best = (G2, U, nw)
         if best is not None:
             G2, U, nw = best
-            eq = equal_chain_plan(g, G, cap, G2, U, nw) if equal_chain else None
+            eq = equal_chain_plan(g, G, cap, G2, U, nw) if (equal_chain and not left) else None
             if eq is not None:
                 return eq
             return dict(G=G2, U=U, ua=U // g.tiles, t1=U % g.tiles, NW=nw, off=0)

@@ -122,6 +122,7 @@ def test_full_size_subset_parity_and_invariants(cuda, oracle_mod, cfg):
 @pytest.mark.parametrize("m,n,k,side,dtype", [
     (512, 512, 64, 0, 0), (4096, 4096, 192, 0, 0), (65536, 2048, 256, 0, 0), (8192, 8192, 128, 0, 1),
     (16384, 16384, 96, 1, 0), (8192, 2048, 256, 0, 0), (16384, 2048, 256, 0, 0), (32768, 2048, 256, 0, 0),
+    (4096, 4096, 192, 1, 0), (4096, 4096, 192, 0, 1),  # left side keeps the aligned plan; fp32 takes equal chains
 ])
 def test_launch_plan_matches_schedule_model(cuda, m, n, k, side, dtype):
     """plan_launch (C++) and the schedule model whose hand-off protocol the CPU suite
@@ -138,7 +139,7 @@ def test_launch_plan_matches_schedule_model(cuda, m, n, k, side, dtype):
     tsz = 8 if dtype == 0 else 4
     cap = warp_cap(tsz, S=2, max_warps=12 if left else 16, left=left)
     owners, length = (n, m) if left else (m, n)
-    pl = plan(Geometry(owners=owners, length=length, k=k), cap=cap)
+    pl = plan(Geometry(owners=owners, length=length, k=k), cap=cap, left=left)
     info = _lib.plan_info(m, n, k, side=side, dtype=dtype)
     assert (info["grid_ctas"], info["warps_per_cta"], info["units"]) == (pl["G"], pl["NW"], pl["U"])
 
